@@ -1,0 +1,336 @@
+/* ORACLE -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+ *
+ * Plain scalar C for the numerics of arXiv 2201.10369's hot path, written from
+ * PAPER.md and SURVEY.md §8(c):
+ *   - canonical fp32 Winograd of one tile, 1D  Y = Aᵀ[(Gg) ⊙ (Bᵀd)]       (eq:conv_1d P:174)
+ *                                          2D  Y = Aᵀ[(GgGᵀ) ⊙ (BᵀdB)]A    (eq:conv_2d P:181)
+ *     every dot product is  acc = +0; for j ascending: acc = fmaf(a_j, b_j, acc)      (O5)
+ *     or, in the paper-arithmetic mode, acc = RN(acc + RN(a_j*b_j))               (O6)
+ *     2D passes: left product first, then right (reading R8);
+ *   - fp64 direct valid cross-correlation of the same fp32 data (eq:conv P:112; O7);
+ *   - error statistics of y32 against y64 ("L1 norm ... normal convolution using
+ *     double precision"; O8);
+ *   - the point sweep (O9) and the tiled multi-channel layer (O4; channel sum in the
+ *     Winograd domain).
+ * No blocking, fusion or reordering beyond the definitions.  Build (see oracle/ref.py):
+ *   gcc -O2 -mfma -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared ref.c -lm
+ * OpenMP runs over independent units only (candidates, tiles, (image, channel)), every
+ * reduction is sequential in a fixed order, so results do not depend on thread count.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OMAXN 16
+
+static inline float mac(float acc, float a, float b, int nofma) {
+  if (nofma) {
+    float p = a * b;   /* RN(a*b); -ffp-contract=off keeps it separate */
+    return acc + p;    /* RN(acc + p) */
+  }
+  return fmaf(a, b, acc);
+}
+
+/* ---------------------------------------------------------------- one tile */
+
+/* 1D: U = G g, V = Bᵀ d, M = U ⊙ V, y = Aᵀ M.  AT[m][n], G[n][r], BT[n][n] row-major. */
+static void tile_1d(int m, int r, const float* AT, const float* G, const float* BT,
+                    const float* d, const float* g, int nofma, float* y) {
+  const int n = m + r - 1;
+  float U[OMAXN], V[OMAXN], M[OMAXN];
+  for (int i = 0; i < n; i++) {
+    float acc = 0.0f;
+    for (int j = 0; j < r; j++) acc = mac(acc, G[i * r + j], g[j], nofma);
+    U[i] = acc;
+  }
+  for (int i = 0; i < n; i++) {
+    float acc = 0.0f;
+    for (int j = 0; j < n; j++) acc = mac(acc, BT[i * n + j], d[j], nofma);
+    V[i] = acc;
+  }
+  for (int i = 0; i < n; i++) M[i] = mac(0.0f, U[i], V[i], nofma);
+  for (int p = 0; p < m; p++) {
+    float acc = 0.0f;
+    for (int i = 0; i < n; i++) acc = mac(acc, AT[p * n + i], M[i], nofma);
+    y[p] = acc;
+  }
+}
+
+/* 2D filter transform U = G g Gᵀ:  T1[i][q] = Σ_j G[i][j] g[j][q];  U[i][l] = Σ_q T1[i][q] G[l][q]. */
+static void filter_2d(int n, int r, const float* G, const float* g, int nofma, float* U) {
+  float T1[OMAXN * OMAXN];
+  for (int i = 0; i < n; i++)
+    for (int q = 0; q < r; q++) {
+      float acc = 0.0f;
+      for (int j = 0; j < r; j++) acc = mac(acc, G[i * r + j], g[j * r + q], nofma);
+      T1[i * r + q] = acc;
+    }
+  for (int i = 0; i < n; i++)
+    for (int l = 0; l < n; l++) {
+      float acc = 0.0f;
+      for (int q = 0; q < r; q++) acc = mac(acc, T1[i * r + q], G[l * r + q], nofma);
+      U[i * n + l] = acc;
+    }
+}
+
+/* 2D input transform V = Bᵀ d B:  T2[i][q] = Σ_j BT[i][j] d[j][q];  V[i][l] = Σ_q T2[i][q] BT[l][q]. */
+static void input_2d(int n, const float* BT, const float* d, int nofma, float* V) {
+  float T2[OMAXN * OMAXN];
+  for (int i = 0; i < n; i++)
+    for (int q = 0; q < n; q++) {
+      float acc = 0.0f;
+      for (int j = 0; j < n; j++) acc = mac(acc, BT[i * n + j], d[j * n + q], nofma);
+      T2[i * n + q] = acc;
+    }
+  for (int i = 0; i < n; i++)
+    for (int l = 0; l < n; l++) {
+      float acc = 0.0f;
+      for (int q = 0; q < n; q++) acc = mac(acc, T2[i * n + q], BT[l * n + q], nofma);
+      V[i * n + l] = acc;
+    }
+}
+
+/* 2D output transform Y = Aᵀ Mw A:  T3[p][l] = Σ_i AT[p][i] Mw[i][l];  Y[p][s] = Σ_l T3[p][l] AT[s][l]. */
+static void output_2d(int m, int n, const float* AT, const float* Mw, int nofma, float* Y) {
+  float T3[OMAXN * OMAXN];
+  for (int p = 0; p < m; p++)
+    for (int l = 0; l < n; l++) {
+      float acc = 0.0f;
+      for (int i = 0; i < n; i++) acc = mac(acc, AT[p * n + i], Mw[i * n + l], nofma);
+      T3[p * n + l] = acc;
+    }
+  for (int p = 0; p < m; p++)
+    for (int s = 0; s < m; s++) {
+      float acc = 0.0f;
+      for (int l = 0; l < n; l++) acc = mac(acc, T3[p * n + l], AT[s * n + l], nofma);
+      Y[p * m + s] = acc;
+    }
+}
+
+static void tile_2d(int m, int r, const float* AT, const float* G, const float* BT,
+                    const float* d, const float* g, int nofma, float* y) {
+  const int n = m + r - 1;
+  float U[OMAXN * OMAXN], V[OMAXN * OMAXN], Mw[OMAXN * OMAXN];
+  filter_2d(n, r, G, g, nofma, U);
+  input_2d(n, BT, d, nofma, V);
+  for (int i = 0; i < n * n; i++) Mw[i] = mac(0.0f, U[i], V[i], nofma);
+  output_2d(m, n, AT, Mw, nofma, y);
+}
+
+/* fp64 direct valid cross-correlation of one tile (O7): products of two fp32 are exact in
+ * fp64; summation ascending u then v. */
+static void direct64_tile(int dims, int m, int r, const float* d, const float* g, double* y) {
+  const int n = m + r - 1;
+  if (dims == 1) {
+    for (int p = 0; p < m; p++) {
+      double acc = 0.0;
+      for (int j = 0; j < r; j++) acc = acc + (double)g[j] * (double)d[p + j];
+      y[p] = acc;
+    }
+  } else {
+    for (int p = 0; p < m; p++)
+      for (int s = 0; s < m; s++) {
+        double acc = 0.0;
+        for (int u = 0; u < r; u++)
+          for (int v = 0; v < r; v++) acc = acc + (double)g[u * r + v] * (double)d[(p + u) * n + (s + v)];
+        y[p * m + s] = acc;
+      }
+  }
+}
+
+/* fp32 direct correlation (the paper's n = 0 rows). */
+static void direct32_tile(int dims, int m, int r, const float* d, const float* g, int nofma, float* y) {
+  const int n = m + r - 1;
+  if (dims == 1) {
+    for (int p = 0; p < m; p++) {
+      float acc = 0.0f;
+      for (int j = 0; j < r; j++) acc = mac(acc, g[j], d[p + j], nofma);
+      y[p] = acc;
+    }
+  } else {
+    for (int p = 0; p < m; p++)
+      for (int s = 0; s < m; s++) {
+        float acc = 0.0f;
+        for (int u = 0; u < r; u++)
+          for (int v = 0; v < r; v++) acc = mac(acc, g[u * r + v], d[(p + u) * n + (s + v)], nofma);
+        y[p * m + s] = acc;
+      }
+  }
+}
+
+/* O8: e = RN64((double)y32 - y64); non-finite e counted and excluded. */
+static inline void stat_acc(double* sums, double* maxs, float y32, double y64) {
+  double e = (double)y32 - y64;
+  if (!isfinite(e)) { sums[4] += 1.0; return; }
+  double ae = fabs(e), ay = fabs(y64);
+  sums[0] += ae;
+  sums[1] += e * e;
+  sums[2] += ay;
+  sums[3] += 1.0;
+  if (ae > maxs[0]) maxs[0] = ae;
+  if (ay > maxs[1]) maxs[1] = ay;
+}
+
+/* ---------------------------------------------------------------- exported API */
+
+int oref_tile(int dims, int m, int r, const float* AT, const float* G, const float* BT,
+              const float* d, const float* g, int nofma, float* y) {
+  if (m < 1 || r < 1 || m + r - 1 > OMAXN) return 1;
+  if (dims == 1) tile_1d(m, r, AT, G, BT, d, g, nofma, y);
+  else if (dims == 2) tile_2d(m, r, AT, G, BT, d, g, nofma, y);
+  else return 1;
+  return 0;
+}
+
+/* y64[t][m^dims] for every tile. */
+int oref_direct64_tiles(int dims, int m, int r, int64_t n_tiles, const float* d_tiles,
+                        const float* g_tiles, double* y64) {
+  const int n = m + r - 1;
+  const int dn = dims == 1 ? n : n * n, dg = dims == 1 ? r : r * r, dy = dims == 1 ? m : m * m;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n_tiles; t++)
+    direct64_tile(dims, m, r, d_tiles + t * dn, g_tiles + t * dg, y64 + t * dy);
+  return 0;
+}
+
+/* O9: per-candidate statistics over all tiles.
+ * mats: per candidate [AT (m*n) | G (n*r) | BT (n*n)] fp32, packed.
+ * direct32 != 0: ignore mats and score the fp32 direct correlation instead (n = 0 row).
+ * sums[n_cand][5], maxs[n_cand][2] are OVERWRITTEN.  y_dump (optional) receives
+ * the outputs of the first n_dump tiles of every candidate: [n_cand][n_dump][m^dims]. */
+int oref_sweep(int dims, int m, int r, int n_cand, const float* mats, int64_t n_tiles,
+               const float* d_tiles, const float* g_tiles, int nofma, int direct32,
+               double* sums, double* maxs, int64_t n_dump, float* y_dump) {
+  const int n = m + r - 1;
+  if (m < 1 || r < 1 || n > OMAXN || (dims != 1 && dims != 2)) return 1;
+  const int dn = dims == 1 ? n : n * n, dg = dims == 1 ? r : r * r, dy = dims == 1 ? m : m * m;
+  const int64_t mstride = (int64_t)m * n + (int64_t)n * r + (int64_t)n * n;
+  double* y64 = (double*)malloc(sizeof(double) * (size_t)(n_tiles > 0 ? n_tiles : 1) * dy);
+  if (!y64) return 2;
+  oref_direct64_tiles(dims, m, r, n_tiles, d_tiles, g_tiles, y64);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int s = 0; s < n_cand; s++) {
+    const float* AT = mats + s * mstride;
+    const float* G = AT + m * n;
+    const float* BT = G + n * r;
+    double* su = sums + 5 * (int64_t)s;
+    double* mx = maxs + 2 * (int64_t)s;
+    for (int i = 0; i < 5; i++) su[i] = 0.0;
+    mx[0] = mx[1] = 0.0;
+    float y[OMAXN * OMAXN];
+    for (int64_t t = 0; t < n_tiles; t++) {
+      const float* d = d_tiles + t * dn;
+      const float* g = g_tiles + t * dg;
+      if (direct32) direct32_tile(dims, m, r, d, g, nofma, y);
+      else if (dims == 1) tile_1d(m, r, AT, G, BT, d, g, nofma, y);
+      else tile_2d(m, r, AT, G, BT, d, g, nofma, y);
+      for (int o = 0; o < dy; o++) stat_acc(su, mx, y[o], y64[t * dy + o]);
+      if (y_dump && t < n_dump)
+        memcpy(y_dump + ((int64_t)s * n_dump + t) * dy, y, sizeof(float) * dy);
+    }
+  }
+  free(y64);
+  return 0;
+}
+
+/* O4 + O5: fp32 Winograd layer, stride 1, symmetric zero padding, NCHW x, KCRS w, NKHW y.
+ * Only images n_lo <= img < n_hi are computed (the rest of y is left untouched).
+ * Channel accumulation in the Winograd domain, ascending c. */
+int oref_conv2d_wino(const float* x, const float* w, float* y, int N, int C, int H, int W, int K,
+                     int r, int pad, int m, const float* AT, const float* G, const float* BT,
+                     int nofma, int n_lo, int n_hi) {
+  const int n = m + r - 1, nn = n * n;
+  if (m < 1 || r < 1 || n > OMAXN || pad < 0) return 1;
+  const int Ho = H + 2 * pad - r + 1, Wo = W + 2 * pad - r + 1;
+  if (Ho < 1 || Wo < 1) return 1;
+  const int th = (Ho + m - 1) / m, tw = (Wo + m - 1) / m;
+  float* U = (float*)malloc(sizeof(float) * (size_t)K * C * nn);
+  if (!U) return 2;
+#pragma omp parallel for schedule(static)
+  for (int64_t kc = 0; kc < (int64_t)K * C; kc++)
+    filter_2d(n, r, G, w + kc * r * r, nofma, U + kc * nn);
+  const int64_t ntile = (int64_t)(n_hi - n_lo) * th * tw;
+  int fail = 0;
+#pragma omp parallel
+  {
+    float* V = (float*)malloc(sizeof(float) * (size_t)C * nn);
+    if (!V) {
+#pragma omp atomic write
+      fail = 1;
+    }
+#pragma omp for schedule(dynamic, 4)
+    for (int64_t it = 0; it < ntile; it++) {
+      if (!V) continue;
+      const int img = n_lo + (int)(it / (th * tw));
+      const int ty = (int)((it / tw) % th), tx = (int)(it % tw);
+      float d[OMAXN * OMAXN], Mw[OMAXN * OMAXN], Y[OMAXN * OMAXN];
+      for (int c = 0; c < C; c++) {
+        const float* xc = x + ((int64_t)img * C + c) * H * W;
+        for (int a = 0; a < n; a++)
+          for (int b = 0; b < n; b++) {
+            const int h = ty * m - pad + a, ww = tx * m - pad + b;
+            d[a * n + b] = (h >= 0 && h < H && ww >= 0 && ww < W) ? xc[(int64_t)h * W + ww] : 0.0f;
+          }
+        input_2d(n, BT, d, nofma, V + (int64_t)c * nn);
+      }
+      for (int k = 0; k < K; k++) {
+        for (int i = 0; i < nn; i++) {
+          float acc = 0.0f;
+          for (int c = 0; c < C; c++) acc = mac(acc, U[((int64_t)k * C + c) * nn + i], V[(int64_t)c * nn + i], nofma);
+          Mw[i] = acc;
+        }
+        output_2d(m, n, AT, Mw, nofma, Y);
+        float* yk = y + ((int64_t)img * K + k) * Ho * Wo;
+        for (int p = 0; p < m; p++)
+          for (int s = 0; s < m; s++) {
+            const int h = ty * m + p, ww = tx * m + s;
+            if (h < Ho && ww < Wo) yk[(int64_t)h * Wo + ww] = Y[p * m + s];
+          }
+      }
+    }
+    free(V);
+  }
+  free(U);
+  return fail ? 2 : 0;
+}
+
+/* O7 for the layer: y64[img][k][h][w] = Σ_c Σ_u Σ_v w·x (ascending), out-of-range x = 0. */
+int oref_conv2d_direct64(const float* x, const float* w, double* y64, int N, int C, int H, int W,
+                         int K, int r, int pad, int n_lo, int n_hi) {
+  const int Ho = H + 2 * pad - r + 1, Wo = W + 2 * pad - r + 1;
+  if (Ho < 1 || Wo < 1) return 1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t ik = (int64_t)n_lo * K; ik < (int64_t)n_hi * K; ik++) {
+    const int img = (int)(ik / K), k = (int)(ik % K);
+    for (int h = 0; h < Ho; h++)
+      for (int ww = 0; ww < Wo; ww++) {
+        double acc = 0.0;
+        for (int c = 0; c < C; c++)
+          for (int u = 0; u < r; u++)
+            for (int v = 0; v < r; v++) {
+              const int hh = h + u - pad, wx = ww + v - pad;
+              if (hh < 0 || hh >= H || wx < 0 || wx >= W) continue;
+              acc = acc + (double)w[(((int64_t)k * C + c) * r + u) * r + v] *
+                              (double)x[(((int64_t)img * C + c) * H + hh) * W + wx];
+            }
+        y64[(((int64_t)img * K + k) * Ho + h) * Wo + ww] = acc;
+      }
+  }
+  return 0;
+}
+
+/* O8 over a flat array, sequential; sums/maxs ACCUMULATE. */
+int oref_stats(const float* y32, const double* y64, int64_t count, double* sums, double* maxs) {
+  for (int64_t i = 0; i < count; i++) stat_acc(sums, maxs, y32[i], y64[i]);
+  return 0;
+}
+
+int oref_max_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
