@@ -1,0 +1,132 @@
+/* wino.h -- C ABI of the B200 (sm_100a) hot path of arXiv 2201.10369
+ * ("symmetric interpolation points for Winograd / Toom-Cook convolution").
+ *
+ * Citations are PAPER.md line numbers (P:n); readings of the paper are numbered
+ * R1.. in DESIGN.md §2.
+ *
+ * Conventions (all calls):
+ *  - Plain C types only.  The caller owns every buffer; the library keeps no pointer
+ *    after a call returns and allocates no device memory (scratch comes from the
+ *    caller's workspace).  No C++ exception crosses the ABI.
+ *  - Return value: WINO_OK or a wino_status.  Argument / shape errors are detected
+ *    synchronously before any device work is enqueued; wino_last_error() then holds a
+ *    thread-local message.  Device faults surface at the caller's next synchronisation.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *    device work is enqueued on it, asynchronously.
+ *  - Matrices are row-major.  Row i of G and Bᵀ, and column i of Aᵀ, belong to
+ *    points[i] (caller order honoured; drivers pass canonical order = finite points
+ *    ascending, +INFINITY last).
+ */
+#ifndef WINO_H_
+#define WINO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  WINO_OK = 0,
+  WINO_E_INVALID_ARG = 1,      /* NULL pointer, m < 1, r < 1, n_cand < 0, dims not 1|2, pad < 0 ... */
+  WINO_E_BAD_SHAPE = 2,        /* n != m + r - 1; empty output (H + 2 pad < r)                       */
+  WINO_E_DUPLICATE_POINTS = 3, /* two finite points compare equal (exact ==; +0 == -0)               */
+  WINO_E_INF_NOT_LAST = 4,     /* +INFINITY anywhere but the last slot, or -INFINITY anywhere        */
+  WINO_E_NONFINITE_POINT = 5,  /* NaN point                                                          */
+  WINO_E_WORKSPACE = 6,        /* workspace NULL or smaller than the *_workspace_bytes() figure      */
+  WINO_E_CUDA = 7,             /* CUDA launch / configuration error (detail in wino_last_error())    */
+  WINO_E_UNSUPPORTED = 8       /* (dims, m, r) without a compiled kernel (see wino_supported())      */
+} wino_status;
+
+#define WINO_MAX_N 16 /* n = m + r - 1 accepted by wino_points_to_matrices */
+
+/* Error statistics ("L1 norm ... between the output of each type of convolution
+ * and a normal convolution using double precision"; per element, reading R10).  fp64,
+ * per scored unit (candidate, or layer):
+ *   sums[5] = { Σ|e|, Σe², Σ|y_ref|, n_scored, n_nonfinite },  maxs[2] = { max|e|, max|y_ref| }
+ * with e = RN64((double)y32 − y64) for every output; non-finite e only increments
+ * n_nonfinite.  Calls ACCUMULATE (sums +=, maxs = max) so buffers can be summed over
+ * calls and all-reduced over ranks; the caller zero-initialises them.
+ * Mean absolute error = sums[0] / sums[3]. */
+#define WINO_SUMS 5
+#define WINO_MAXS 2
+
+/* Sweep flags. */
+#define WINO_SWEEP_NOFMA 1u /* paper arithmetic acc = RN(acc + RN(a*b)) instead of fmaf chains (R13) */
+
+const char* wino_status_string(int status);
+const char* wino_last_error(void);
+/* 1 if a kernel for (dims, m, r) is compiled into this library, else 0. */
+int wino_supported(int dims, int m, int r);
+
+/* (1) Points -> transform matrices.  Host only, synchronous, pure, thread-safe.
+ *
+ * Defines (§4.1; §4.2 modified algorithm):
+ *   Aᵀ[p][i] = αᵢ^p (m x n), G[i][q] = αᵢ^q / Nᵢ with Nᵢ = ∏_{j≠i}(αᵢ − αⱼ) (n x r; the
+ *   scaling factor is DIVIDED, reading R1), Bᵀ row i = ascending coefficients of
+ *   Mᵢ(x) = ∏_{j≠i}(x − αⱼ) (n x n).  If points[n-1] == +INFINITY (modified Toom-Cook):
+ *   the products run over the n-1 finite points, G's last row is [0..0 1], Aᵀ's last
+ *   column is [0..0 1]ᵀ, Bᵀ's last row holds the coefficients of M′(x) = ∏ⱼ(x − αⱼ) and
+ *   its last column is [0..0 1]ᵀ (reading R4).
+ * Arithmetic: the fixed fp64 recipe R64: every entry is bit-identical
+ * to the oracle's.  points: HOST double[n], n = m + r − 1 ≤ WINO_MAX_N.
+ * AT: HOST double[m*n], G: HOST double[n*r], BT: HOST double[n*n] (caller-allocated,
+ * fully overwritten on success, untouched on error).
+ * Errors: INVALID_ARG, BAD_SHAPE, DUPLICATE_POINTS, INF_NOT_LAST, NONFINITE_POINT,
+ * UNSUPPORTED (n > WINO_MAX_N). */
+int wino_points_to_matrices(int m, int r, const double* points, int n,
+                            double* AT, double* G, double* BT);
+
+/* (2) fp32 Winograd convolution layer F(m x m, r x r), stride 1, symmetric zero padding
+ * `pad`, no bias (eq:conv P:112 read as valid cross-correlation, R3; eq:conv_2d P:181;
+ * channel sum in the Winograd domain).
+ *   x: DEVICE float[N][C][H][W]  w: DEVICE float[K][C][r][r]
+ *   y: DEVICE float[N][K][Ho][Wo], Ho = H + 2 pad − r + 1, Wo = W + 2 pad − r + 1
+ *   points: HOST double[m + r − 1] (rules of (1)); the fp32 matrices are RN32 of (1).
+ *   workspace: DEVICE, >= wino_conv2d_workspace_bytes(...) bytes, 256-byte aligned.
+ *   d_sums / d_maxs: DEVICE double[WINO_SUMS] / double[WINO_MAXS], or both NULL.  When
+ *   non-NULL every output is also scored against the fp64 direct convolution of the same
+ *   fp32 x, w and the statistics are ACCUMULATED into them.
+ * Arithmetic (the parity semantics, DESIGN.md §2.3 "F32-FMA"): each dot product is an
+ * ascending fmaf chain from +0; 2D transforms left product first; the channel sum is one
+ * ascending-c fmaf chain per (k, tile, Winograd position), no split, no TF32.
+ * Output is bit-identical to the oracle's O5 layer.  Asynchronous on `stream`. */
+size_t wino_conv2d_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m);
+int wino_conv2d_fp32(const float* x, const float* w, float* y,
+                     int N, int C, int H, int W, int K, int r, int pad, int m,
+                     const double* points, void* workspace, size_t workspace_bytes,
+                     double* d_sums, double* d_maxs, void* stream);
+
+/* (3) Error sweep over candidate point sets on ONE device (P:465 error protocol; P:472
+ * sweep; the multi-GPU driver shards candidates over ranks and all-reduces the stats).
+ *   dims 1|2; point_sets: HOST double[n_cand][n] (each row obeys (1)).
+ *   d_tiles: DEVICE float[n_tiles][n^dims], g_tiles: DEVICE float[n_tiles][r^dims]
+ *   (row-major n x n / r x r tiles; the SAME tiles score every candidate, O9).
+ *   d_sums: DEVICE double[n_cand][WINO_SUMS], d_maxs: DEVICE double[n_cand][WINO_MAXS]
+ *   (ACCUMULATED).  cand_status: HOST int[n_cand] out, per-candidate wino_status of (1);
+ *   a rejected candidate is skipped (its stats untouched) and does not fail the call.
+ *   workspace: DEVICE, >= wino_error_sweep_workspace_bytes(...).  flags: WINO_SWEEP_*.
+ * Every output of every tile is scored against the fp64 direct correlation of the tile.
+ * Asynchronous on `stream` (host matrix construction happens before the launch). */
+size_t wino_error_sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles);
+int wino_error_sweep(int dims, int m, int r, const double* point_sets, int n_cand,
+                     const float* d_tiles, const float* g_tiles, int64_t n_tiles,
+                     double* d_sums, double* d_maxs, int* cand_status,
+                     void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
+
+/* (3b) The sweep's fp32 outputs themselves (same kernel code path as (3), scoring off):
+ *   d_y: DEVICE float[n_cand][n_tiles][m^dims].  Rejected candidates' rows are untouched.
+ * Used for per-element parity against the oracle. */
+int wino_sweep_outputs(int dims, int m, int r, const double* point_sets, int n_cand,
+                       const float* d_tiles, const float* g_tiles, int64_t n_tiles,
+                       float* d_y, int* cand_status, unsigned flags, void* stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued
+ * (for bench.py's gpu_launches count). */
+int wino_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WINO_H_ */

@@ -1,0 +1,160 @@
+// The C ABI of libwino (include/wino.h): validation, host matrix construction, launch.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "wino_internal.h"
+
+namespace wino {
+
+namespace {
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+thread_local int g_last_launches = 0;
+}  // namespace
+
+int set_error(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+void count_launches(int n) { g_launches += n; }
+void reset_launches() { g_launches = 0; }
+
+}  // namespace wino
+
+using namespace wino;
+
+namespace {
+int finish(int status) {
+  if (status == WINO_OK) g_last_launches = g_launches;
+  return status;
+}
+
+// RN32 of the R64 matrices.
+void to_f32(const double* src, int count, float* dst) {
+  for (int i = 0; i < count; i++) dst[i] = (float)src[i];
+}
+}  // namespace
+
+extern "C" {
+
+const char* wino_status_string(int status) {
+  switch (status) {
+    case WINO_OK: return "WINO_OK";
+    case WINO_E_INVALID_ARG: return "WINO_E_INVALID_ARG";
+    case WINO_E_BAD_SHAPE: return "WINO_E_BAD_SHAPE";
+    case WINO_E_DUPLICATE_POINTS: return "WINO_E_DUPLICATE_POINTS";
+    case WINO_E_INF_NOT_LAST: return "WINO_E_INF_NOT_LAST";
+    case WINO_E_NONFINITE_POINT: return "WINO_E_NONFINITE_POINT";
+    case WINO_E_WORKSPACE: return "WINO_E_WORKSPACE";
+    case WINO_E_CUDA: return "WINO_E_CUDA";
+    case WINO_E_UNSUPPORTED: return "WINO_E_UNSUPPORTED";
+    default: return "WINO_E_UNKNOWN";
+  }
+}
+
+const char* wino_last_error(void) { return g_err; }
+
+int wino_last_launch_count(void) { return g_last_launches; }
+
+int wino_supported(int dims, int m, int r) {
+  if (dims == 1 || dims == 2) return sweep_supported(dims, m, r);
+  if (dims == 0) return layer_supported(m, r);  // 0 = the layer kernels
+  return 0;
+}
+
+int wino_points_to_matrices(int m, int r, const double* points, int n, double* AT, double* G, double* BT) {
+  const int s = build_r64(m, r, points, n, AT, G, BT);
+  if (s != WINO_OK) return set_error(s, "wino_points_to_matrices: %s", build_error_detail(s));
+  return WINO_OK;
+}
+
+size_t wino_conv2d_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m) {
+  if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || r < 1 || m < 1 || pad < 0) return 0;
+  if (H + 2 * pad < r || W + 2 * pad < r) return 0;
+  return layer_workspace_bytes(N, C, H, W, K, r, pad, m);
+}
+
+int wino_conv2d_fp32(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
+                     int m, const double* points, void* workspace, size_t workspace_bytes, double* d_sums,
+                     double* d_maxs, void* stream) {
+  reset_launches();
+  if (!x || !w || !y || !points) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || r < 1 || m < 1 || pad < 0)
+    return set_error(WINO_E_INVALID_ARG, "non-positive size or negative pad");
+  if ((d_sums == nullptr) != (d_maxs == nullptr))
+    return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
+  if (H + 2 * pad < r || W + 2 * pad < r) return set_error(WINO_E_BAD_SHAPE, "empty output");
+  const int n = m + r - 1;
+  if (n > WINO_MAX_N) return set_error(WINO_E_UNSUPPORTED, "n > WINO_MAX_N");
+  if (!layer_supported(m, r)) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
+  std::vector<double> AT(m * n), G(n * r), BT(n * n);
+  const int s = build_r64(m, r, points, n, AT.data(), G.data(), BT.data());
+  if (s != WINO_OK) return set_error(s, "points: %s", build_error_detail(s));
+  std::vector<float> ATf(m * n), Gf(n * r), BTf(n * n);
+  to_f32(AT.data(), m * n, ATf.data());
+  to_f32(G.data(), n * r, Gf.data());
+  to_f32(BT.data(), n * n, BTf.data());
+  return finish(layer_launch(x, w, y, N, C, H, W, K, r, pad, m, ATf.data(), Gf.data(), BTf.data(), workspace,
+                             workspace_bytes, d_sums, d_maxs, (cudaStream_t)stream));
+}
+
+size_t wino_error_sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles) {
+  if ((dims != 1 && dims != 2) || m < 1 || r < 1 || n_cand < 0 || n_tiles < 0) return 0;
+  return sweep_workspace_bytes(dims, m, r, n_cand, n_tiles);
+}
+
+static int sweep_common(int dims, int m, int r, const double* point_sets, int n_cand, const float* d_tiles,
+                        const float* g_tiles, int64_t n_tiles, double* d_sums, double* d_maxs, float* d_y,
+                        int* cand_status, void* workspace, size_t ws_bytes, unsigned flags, void* stream) {
+  reset_launches();
+  if (dims != 1 && dims != 2) return set_error(WINO_E_INVALID_ARG, "dims must be 1 or 2");
+  if (m < 1 || r < 1 || n_cand < 0 || n_tiles < 0) return set_error(WINO_E_INVALID_ARG, "bad sizes");
+  if (n_cand > 0 && (!point_sets || !cand_status)) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  if (n_cand > 0 && n_tiles > 0 && (!d_tiles || !g_tiles)) return set_error(WINO_E_INVALID_ARG, "NULL tiles");
+  if (!d_y && n_cand > 0 && (!d_sums || !d_maxs)) return set_error(WINO_E_INVALID_ARG, "NULL stats");
+  if (flags & ~WINO_SWEEP_NOFMA) return set_error(WINO_E_INVALID_ARG, "unknown flags");
+  const int n = m + r - 1;
+  if (n > WINO_MAX_N) return set_error(WINO_E_UNSUPPORTED, "n > WINO_MAX_N");
+  if (!sweep_supported(dims, m, r))
+    return set_error(WINO_E_UNSUPPORTED, "no sweep kernel for dims=%d m=%d r=%d", dims, m, r);
+  const int per = m * n + n * r + n * n;
+  std::vector<float> mats((size_t)(n_cand > 0 ? n_cand : 1) * per);
+  std::vector<int> ok(n_cand > 0 ? n_cand : 1);
+  std::vector<double> AT(m * n), G(n * r), BT(n * n);
+  for (int c = 0; c < n_cand; c++) {
+    const int s = build_r64(m, r, point_sets + (size_t)c * n, n, AT.data(), G.data(), BT.data());
+    cand_status[c] = s;
+    ok[c] = s == WINO_OK;
+    if (s == WINO_OK) {
+      float* dst = mats.data() + (size_t)c * per;
+      to_f32(AT.data(), m * n, dst);
+      to_f32(G.data(), n * r, dst + m * n);
+      to_f32(BT.data(), n * n, dst + m * n + n * r);
+    }
+  }
+  return finish(sweep_launch(dims, m, r, mats.data(), ok.data(), n_cand, d_tiles, g_tiles, n_tiles, d_sums, d_maxs,
+                             d_y, workspace, ws_bytes, flags, (cudaStream_t)stream));
+}
+
+int wino_error_sweep(int dims, int m, int r, const double* point_sets, int n_cand, const float* d_tiles,
+                     const float* g_tiles, int64_t n_tiles, double* d_sums, double* d_maxs, int* cand_status,
+                     void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  return sweep_common(dims, m, r, point_sets, n_cand, d_tiles, g_tiles, n_tiles, d_sums, d_maxs, nullptr,
+                      cand_status, workspace, workspace_bytes, flags, stream);
+}
+
+int wino_sweep_outputs(int dims, int m, int r, const double* point_sets, int n_cand, const float* d_tiles,
+                       const float* g_tiles, int64_t n_tiles, float* d_y, int* cand_status, unsigned flags,
+                       void* stream) {
+  if (!d_y && n_cand > 0 && n_tiles > 0) return set_error(WINO_E_INVALID_ARG, "NULL d_y");
+  return sweep_common(dims, m, r, point_sets, n_cand, d_tiles, g_tiles, n_tiles, nullptr, nullptr,
+                      d_y ? d_y : nullptr, cand_status, nullptr, 0, flags, stream);
+}
+
+}  // extern "C"

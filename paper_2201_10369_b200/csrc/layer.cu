@@ -1,0 +1,469 @@
+// fp32 Winograd convolution layer F(m x m, r x r) (PAPER.md eq:conv_2d P:181; the channel
+// sum "implemented using matrix multiplication"), sm_100a.  Kernels:
+//   K1 filter_kernel : U_p[c][k] = (G w_kc Gᵀ)[p]                     -> U [NN][Cp][Kp]
+//   K2 input_kernel  : V_p[c][t] = (Bᵀ d_ct B)[p], zero padding        -> V [NN][Cp][Tp]
+//   K3 gemm_kernel   : M_p[k][t] = Σ_c U_p[c][k] V_p[c][t]  (NN batched fp32 GEMMs,
+//                      FFMA2 register tiles, ascending-c chain, no split-K, no TF32)
+//   K4 output_kernel : y tile = Aᵀ M_t A, cropped                      -> y [N][K][Ho][Wo]
+//   K5 score_kernel  : y64 = fp64 direct correlation (eq:conv P:112), e = y - y64,
+//                      per-warp statistics (warp shuffles), fixed grid
+//   K8 finalize      : fixed-order reduction into d_sums/d_maxs
+// Cp = C rounded up to 8, Kp = K and Tp = T rounded up to 128; padding is zero-filled
+// by K1/K2, so K3 needs no bounds checks (an fma(0, 0, acc) leaves acc unchanged up to
+// the sign of a zero).  Parity semantics: every dot product is an
+// fmaf chain from +0 in ascending index order, 2D transforms left product first.
+#include <algorithm>
+#include <cstdio>
+
+#include "wino_internal.h"
+
+namespace wino {
+
+namespace {
+
+typedef unsigned long long u64;
+
+constexpr int kMaxN = 10;   // layer kernels compiled for n <= 10
+
+struct LayerMats {
+  float AT[kMaxN * kMaxN];  // [m][n]
+  float G[kMaxN * kMaxN];   // [n][r]
+  float BT[kMaxN * kMaxN];  // [n][n]
+};
+
+struct Geo {
+  int N, C, H, W, K, r, pad, m;
+  int Ho, Wo, th, tw;
+  long long T;     // tiles = N * th * tw
+  int Cp, Kp;
+  long long Tp;
+};
+
+Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m) {
+  Geo g;
+  g.N = N; g.C = C; g.H = H; g.W = W; g.K = K; g.r = r; g.pad = pad; g.m = m;
+  g.Ho = H + 2 * pad - r + 1;
+  g.Wo = W + 2 * pad - r + 1;
+  g.th = (g.Ho + m - 1) / m;
+  g.tw = (g.Wo + m - 1) / m;
+  g.T = (long long)N * g.th * g.tw;
+  g.Cp = (C + 7) / 8 * 8;
+  g.Kp = (K + 127) / 128 * 128;
+  g.Tp = (g.T + 127) / 128 * 128;
+  return g;
+}
+
+constexpr int kScoreBlocks = 1184;   // fixed grid (8 x 148) -> deterministic partition
+constexpr int kScoreThreads = 256;
+
+// ------------------------------------------------------------------ K1
+template <int M, int R>
+__global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U, int C, int K, int Cp, int Kp,
+                              const __grid_constant__ LayerMats mt) {
+  constexpr int N = M + R - 1;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp * Kp, k fastest
+  if (idx >= (long long)Cp * Kp) return;
+  const int k = (int)(idx % Kp), c = (int)(idx / Kp);
+  const long long plane = (long long)Cp * Kp;
+  if (k >= K || c >= C) {
+#pragma unroll
+    for (int p = 0; p < N * N; p++) U[p * plane + idx] = 0.0f;
+    return;
+  }
+  float g[R * R];
+  const float* wk = w + ((long long)k * C + c) * R * R;
+#pragma unroll
+  for (int e = 0; e < R * R; e++) g[e] = wk[e];
+  float t1[N][R];
+#pragma unroll
+  for (int i = 0; i < N; i++)
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < R; j++) acc = __fmaf_rn(mt.G[i * R + j], g[j * R + q], acc);
+      t1[i][q] = acc;
+    }
+#pragma unroll
+  for (int i = 0; i < N; i++)
+#pragma unroll
+    for (int l = 0; l < N; l++) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < R; q++) acc = __fmaf_rn(t1[i][q], mt.G[l * R + q], acc);
+      U[(i * N + l) * plane + idx] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ K2
+// one thread per (c, t); t fastest -> coalesced V stores per Winograd position
+template <int M, int R>
+__global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V, Geo geo,
+                             const __grid_constant__ LayerMats mt) {
+  constexpr int N = M + R - 1;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp * Tp
+  if (idx >= (long long)geo.Cp * geo.Tp) return;
+  const long long t = idx % geo.Tp;
+  const int c = (int)(idx / geo.Tp);
+  const long long plane = (long long)geo.Cp * geo.Tp;
+  if (t >= geo.T || c >= geo.C) {
+#pragma unroll
+    for (int p = 0; p < N * N; p++) V[p * plane + idx] = 0.0f;
+    return;
+  }
+  const int per_img = geo.th * geo.tw;
+  const int img = (int)(t / per_img);
+  const int rem = (int)(t - (long long)img * per_img);
+  const int ty = rem / geo.tw, tx = rem - ty * geo.tw;
+  const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
+  const int h0 = ty * M - geo.pad, w0 = tx * M - geo.pad;
+  float d[N][N];
+#pragma unroll
+  for (int a = 0; a < N; a++)
+#pragma unroll
+    for (int b = 0; b < N; b++) {
+      const int h = h0 + a, ww = w0 + b;
+      d[a][b] = (h >= 0 && h < geo.H && ww >= 0 && ww < geo.W) ? __ldg(xc + (long long)h * geo.W + ww) : 0.0f;
+    }
+  // T2[i][q] = Σ_j Bᵀ[i][j] d[j][q]
+  float t2[N][N];
+#pragma unroll
+  for (int q = 0; q < N; q++)
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < N; j++) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
+      t2[i][q] = acc;
+    }
+  // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
+#pragma unroll
+  for (int i = 0; i < N; i++)
+#pragma unroll
+    for (int l = 0; l < N; l++) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
+      V[(i * N + l) * plane + idx] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ K3
+// Batched SGEMM  M_p[k][t] = Σ_c U_p[c][k] V_p[c][t], 128 x 128 CTA tile, BK = 8,
+// 256 threads x (8 x 8) register tile, accumulators as FFMA2 pairs along t.
+// cp.async double-buffered shared memory; every accumulator is one ascending-c fmaf chain.
+constexpr int BM = 128, BN = 128, BK = 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NW>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
+
+__device__ __forceinline__ u64 ffma2_bcast(u64 a, float c, u64 acc) {
+  u64 d, cc;
+  asm("mov.b64 %0, {%1,%1};" : "=l"(cc) : "f"(c));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(cc), "l"(acc));
+  return d;
+}
+
+__global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ U, const float* __restrict__ V,
+                                                      float* __restrict__ Mo, int Cp, int Kp, long long Tp) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const long long t0 = (long long)blockIdx.x * BN;
+  const int k0 = blockIdx.y * BM;
+  const int p = blockIdx.z;
+  const float* Ap = U + (long long)p * Cp * Kp + k0;
+  const float* Bp = V + (long long)p * Cp * Tp + t0;
+  // loader mapping: 256 threads x float4 = 8 rows x 128 columns
+  const int lr = tid >> 5, lc = (tid & 31) * 4;
+
+  u64 acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
+
+  const int nk = Cp / BK;
+  cp_async16(&As[0][lr][lc], Ap + (long long)lr * Kp + lc);
+  cp_async16(&Bs[0][lr][lc], Bp + (long long)lr * Tp + lc);
+  cp_async_commit();
+  for (int kt = 0; kt < nk; kt++) {
+    const int cur = kt & 1;
+    if (kt + 1 < nk) {
+      const long long c1 = (long long)(kt + 1) * BK + lr;
+      cp_async16(&As[cur ^ 1][lr][lc], Ap + c1 * Kp + lc);
+      cp_async16(&Bs[cur ^ 1][lr][lc], Bp + c1 * Tp + lc);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; kk++) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][64 + ty * 4]);
+      const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][tx * 4]);
+      const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const u64 b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = ffma2_bcast(b[j], a[i], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* Mp = Mo + (long long)p * Kp * Tp;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int k = k0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    float* row = Mp + (long long)k * Tp + t0;
+    *reinterpret_cast<ulonglong2*>(row + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
+    *reinterpret_cast<ulonglong2*>(row + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
+  }
+}
+
+// ------------------------------------------------------------------ K4
+// one thread per (k, t); t fastest -> coalesced M loads per Winograd position
+template <int M, int R>
+__global__ void output_kernel(const float* __restrict__ Mw, float* __restrict__ y, Geo geo,
+                              const __grid_constant__ LayerMats mt) {
+  constexpr int N = M + R - 1;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * T
+  if (idx >= (long long)geo.K * geo.T) return;
+  const long long t = idx % geo.T;
+  const int k = (int)(idx / geo.T);
+  const long long plane = (long long)geo.Kp * geo.Tp;
+  const float* src = Mw + (long long)k * geo.Tp + t;
+  float mw[N][N];
+#pragma unroll
+  for (int i = 0; i < N; i++)
+#pragma unroll
+    for (int l = 0; l < N; l++) mw[i][l] = src[(i * N + l) * plane];
+  // T3[p][l] = Σ_i Aᵀ[p][i] Mw[i][l]
+  float t3[M][N];
+#pragma unroll
+  for (int p = 0; p < M; p++)
+#pragma unroll
+    for (int l = 0; l < N; l++) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < N; i++) acc = __fmaf_rn(mt.AT[p * N + i], mw[i][l], acc);
+      t3[p][l] = acc;
+    }
+  const int per_img = geo.th * geo.tw;
+  const int img = (int)(t / per_img);
+  const int rem = (int)(t - (long long)img * per_img);
+  const int ty = rem / geo.tw, tx = rem - ty * geo.tw;
+  float* yk = y + ((long long)img * geo.K + k) * geo.Ho * geo.Wo;
+#pragma unroll
+  for (int p = 0; p < M; p++) {
+    const int h = ty * M + p;
+#pragma unroll
+    for (int s = 0; s < M; s++) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int l = 0; l < N; l++) acc = __fmaf_rn(t3[p][l], mt.AT[s * N + l], acc);
+      const int ww = tx * M + s;
+      if (h < geo.Ho && ww < geo.Wo) yk[(long long)h * geo.Wo + ww] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5 scoring
+struct SStat {
+  double s0 = 0, s1 = 0, s2 = 0, m0 = 0, m1 = 0;
+  long long n = 0, nonfin = 0;
+};
+
+__global__ void __launch_bounds__(kScoreThreads) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                              const float* __restrict__ y, Geo geo,
+                                                              double* __restrict__ partial) {
+  const long long total = (long long)geo.N * geo.K * geo.Ho * geo.Wo;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  SStat st;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += stride) {
+    const int ww = (int)(o % geo.Wo);
+    const int h = (int)((o / geo.Wo) % geo.Ho);
+    const int k = (int)((o / ((long long)geo.Wo * geo.Ho)) % geo.K);
+    const int img = (int)(o / ((long long)geo.Wo * geo.Ho * geo.K));
+    double acc = 0.0;
+    for (int c = 0; c < geo.C; c++) {
+      const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
+      const float* wk = w + ((long long)k * geo.C + c) * geo.r * geo.r;
+      for (int u = 0; u < geo.r; u++) {
+        const int hh = h + u - geo.pad;
+        if (hh < 0 || hh >= geo.H) continue;
+        for (int v = 0; v < geo.r; v++) {
+          const int wx = ww + v - geo.pad;
+          if (wx < 0 || wx >= geo.W) continue;
+          acc = __fma_rn((double)__ldg(wk + u * geo.r + v), (double)__ldg(xc + (long long)hh * geo.W + wx), acc);
+        }
+      }
+    }
+    const double e = (double)y[o] - acc;
+    if (isfinite(e)) {
+      st.s0 += fabs(e);
+      st.s1 = __fma_rn(e, e, st.s1);
+      st.s2 += fabs(acc);
+      st.m0 = fmax(st.m0, fabs(e));
+      st.m1 = fmax(st.m1, fabs(acc));
+      st.n++;
+    } else {
+      st.nonfin++;
+    }
+  }
+  double v[7] = {st.s0, st.s1, st.s2, (double)st.n, (double)st.nonfin, st.m0, st.m1};
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int f = 0; f < 5; f++) v[f] += __shfl_xor_sync(0xffffffffu, v[f], off);
+    v[5] = fmax(v[5], __shfl_xor_sync(0xffffffffu, v[5], off));
+    v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    double* p = partial + ((long long)blockIdx.x * (kScoreThreads / 32) + (threadIdx.x >> 5)) * 8;
+#pragma unroll
+    for (int f = 0; f < 7; f++) p[f] = v[f];
+    p[7] = 0.0;
+  }
+}
+
+__global__ void score_finalize_kernel(const double* __restrict__ partial, int n_entries, double* d_sums,
+                                      double* d_maxs) {
+  const int lane = threadIdx.x;
+  double v[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int e = lane; e < n_entries; e += 32) {
+#pragma unroll
+    for (int f = 0; f < 5; f++) v[f] += partial[e * 8 + f];
+    v[5] = fmax(v[5], partial[e * 8 + 5]);
+    v[6] = fmax(v[6], partial[e * 8 + 6]);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int f = 0; f < 5; f++) v[f] += __shfl_xor_sync(0xffffffffu, v[f], off);
+    v[5] = fmax(v[5], __shfl_xor_sync(0xffffffffu, v[5], off));
+    v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
+  }
+  if (lane == 0) {
+    for (int f = 0; f < 5; f++) d_sums[f] += v[f];
+    d_maxs[0] = fmax(d_maxs[0], v[5]);
+    d_maxs[1] = fmax(d_maxs[1], v[6]);
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+typedef void (*FilterK)(const float*, float*, int, int, int, int, LayerMats);
+typedef void (*InputK)(const float*, float*, Geo, LayerMats);
+typedef void (*OutputK)(const float*, float*, Geo, LayerMats);
+
+struct LayerCfg {
+  int m, r;
+  FilterK fk;
+  InputK ik;
+  OutputK ok;
+};
+
+template <int M, int R>
+LayerCfg make_layer_cfg() {
+  return LayerCfg{M, R, filter_kernel<M, R>, input_kernel<M, R>, output_kernel<M, R>};
+}
+
+const LayerCfg kLayerCfgs[] = {
+    make_layer_cfg<2, 3>(), make_layer_cfg<3, 3>(), make_layer_cfg<4, 3>(), make_layer_cfg<5, 3>(),
+    make_layer_cfg<6, 3>(), make_layer_cfg<2, 5>(), make_layer_cfg<4, 5>(), make_layer_cfg<6, 5>(),
+};
+
+const LayerCfg* find_layer(int m, int r) {
+  for (const auto& c : kLayerCfgs)
+    if (c.m == m && c.r == r) return &c;
+  return nullptr;
+}
+
+struct WsLayout {
+  size_t u_off, v_off, m_off, p_off, total;
+};
+
+WsLayout ws_layout(const Geo& g) {
+  const int n = g.m + g.r - 1, nn = n * n;
+  WsLayout L;
+  L.u_off = 0;
+  L.v_off = L.u_off + align_up((size_t)nn * g.Cp * g.Kp * sizeof(float), 256);
+  L.m_off = L.v_off + align_up((size_t)nn * g.Cp * g.Tp * sizeof(float), 256);
+  L.p_off = L.m_off + align_up((size_t)nn * g.Kp * g.Tp * sizeof(float), 256);
+  L.total = L.p_off + align_up((size_t)kScoreBlocks * (kScoreThreads / 32) * 8 * sizeof(double), 256);
+  return L;
+}
+
+}  // namespace
+
+int layer_supported(int m, int r) { return find_layer(m, r) != nullptr; }
+
+size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m) {
+  return ws_layout(make_geo(N, C, H, W, K, r, pad, m)).total;
+}
+
+int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
+                 int m, const float* AT, const float* G, const float* BT, void* workspace, size_t ws_bytes,
+                 double* d_sums, double* d_maxs, cudaStream_t stream) {
+  const LayerCfg* cfg = find_layer(m, r);
+  if (!cfg) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
+  const Geo g = make_geo(N, C, H, W, K, r, pad, m);
+  const WsLayout L = ws_layout(g);
+  if (!workspace || ws_bytes < L.total)
+    return set_error(WINO_E_WORKSPACE, "layer workspace %zu < %zu bytes", ws_bytes, L.total);
+  const int n = m + r - 1;
+  LayerMats mt;
+  std::fill(mt.AT, mt.AT + kMaxN * kMaxN, 0.0f);
+  std::fill(mt.G, mt.G + kMaxN * kMaxN, 0.0f);
+  std::fill(mt.BT, mt.BT + kMaxN * kMaxN, 0.0f);
+  std::copy(AT, AT + m * n, mt.AT);
+  std::copy(G, G + n * r, mt.G);
+  std::copy(BT, BT + n * n, mt.BT);
+  char* ws = reinterpret_cast<char*>(workspace);
+  float* U = reinterpret_cast<float*>(ws + L.u_off);
+  float* V = reinterpret_cast<float*>(ws + L.v_off);
+  float* Mw = reinterpret_cast<float*>(ws + L.m_off);
+  double* partial = reinterpret_cast<double*>(ws + L.p_off);
+  const int tpb = 256;
+  int launches = 0;
+  {
+    const long long tot = (long long)g.Cp * g.Kp;
+    cfg->fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(w, U, C, K, g.Cp, g.Kp, mt);
+    launches++;
+  }
+  {
+    const long long tot = (long long)g.Cp * g.Tp;
+    cfg->ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt);
+    launches++;
+  }
+  {
+    dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
+    gemm_kernel<<<grid, 256, 0, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+    launches++;
+  }
+  {
+    const long long tot = (long long)g.K * g.T;
+    cfg->ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt);
+    launches++;
+  }
+  if (d_sums) {
+    score_kernel<<<kScoreBlocks, kScoreThreads, 0, stream>>>(x, w, y, g, partial);
+    score_finalize_kernel<<<1, 32, 0, stream>>>(partial, kScoreBlocks * (kScoreThreads / 32), d_sums, d_maxs);
+    launches += 2;
+  }
+  count_launches(launches);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(WINO_E_CUDA, "layer launch: %s", cudaGetErrorString(e));
+  return WINO_OK;
+}
+
+}  // namespace wino

@@ -1,0 +1,44 @@
+// Internal helpers shared by the sm_100a kernels and the C ABI of libwino.
+// Nothing here is visible across the ABI (include/wino.h is the boundary).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "../../include/wino.h"
+
+namespace wino {
+
+// ---- host-side status plumbing (capi.cpp) ---------------------------------------
+int set_error(int status, const char* fmt, ...);
+void count_launches(int n);   // adds to the per-call launch counter
+void reset_launches();
+
+// ---- host fp64 matrix builder, recipe R64 (host_builder.cpp) ----------------------
+// Validates (m, r, points) and fills AT[m*n], G[n*r], BT[n*n].  Returns a wino_status,
+// without touching the thread's last-error message (callers decide).
+int build_r64(int m, int r, const double* points, int n, double* AT, double* G, double* BT);
+const char* build_error_detail(int status);
+
+// ---- launchers (sweep.cu, layer.cu) ------------------------------------------------
+// fp32 matrices of one candidate, packed [AT (m*n) | G (n*r) | BT (n*n)].
+int sweep_supported(int dims, int m, int r);
+int sweep_max_cands_per_launch(int dims, int m, int r);
+size_t sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles);
+// Launches K6 (refs) once, then K7+K8 per chunk of candidates.  mats: HOST fp32
+// [n_cand][per]; cand_ok: HOST (skip where 0).
+int sweep_launch(int dims, int m, int r, const float* mats, const int* cand_ok, int n_cand,
+                 const float* d_tiles, const float* g_tiles, int64_t n_tiles,
+                 double* d_sums, double* d_maxs, float* d_y, void* workspace, size_t ws_bytes,
+                 unsigned flags, cudaStream_t stream);
+
+int layer_supported(int m, int r);
+size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m);
+int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K,
+                 int r, int pad, int m, const float* AT, const float* G, const float* BT,
+                 void* workspace, size_t ws_bytes, double* d_sums, double* d_maxs,
+                 cudaStream_t stream);
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace wino

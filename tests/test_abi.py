@@ -1,0 +1,129 @@
+"""C-ABI library: loads, exports every symbol include/wino.h declares, and its host
+matrix builder (wino_points_to_matrices) is bit-identical to the oracle's R64 recipe
+on every point set the configs use plus random sets.  CPU only (no device calls)."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import points as OP, r64
+from paper_2201_10369_b200 import _lib, api, points as PP
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INF = math.inf
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "wino.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(wino_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_header_symbols():
+    L = _lib.load()
+    names = _header_functions()
+    assert len(names) >= 9
+    for n in names:
+        assert hasattr(L, n), n
+    declared = {s[0] for s in _lib.SIGNATURES}
+    assert set(names) == declared
+
+
+def test_status_strings():
+    L = _lib.load()
+    for s in range(9):
+        assert L.wino_status_string(s).decode().startswith("WINO_")
+
+
+def _same_bits(a, b):
+    return np.array_equal(np.asarray(a).view(np.int64), np.asarray(b).view(np.int64))
+
+
+def _check(m, r, pts):
+    got = api.wino_points_to_matrices(m, r, pts)
+    exp = r64.build_r64(m, r, pts)
+    for g, e in zip(got, exp):
+        assert _same_bits(g, e), (m, r, pts)
+
+
+def test_builder_bitexact_cfg1_cfg3_sets():
+    _check(2, 3, [-1.0, 0.0, 1.0, INF])
+    _check(6, 3, PP.family_n8_cd(2.0, 1.003))
+    _check(6, 3, PP.P8)
+    _check(8, 3, PP.P10)
+
+
+def test_builder_bitexact_cfg2_grid():
+    for c in synth.c_grid():
+        _check(4, 3, PP.family_f43(float(c)))
+
+
+def test_builder_bitexact_cfg4_subgrid():
+    g = synth.c_grid(256)
+    for c1 in g[::9]:
+        for c2 in g[::11]:
+            for m, maker in ((4, PP.family_n8_c1c2), (6, PP.family_n10)):
+                try:
+                    pts = maker(float(c1), float(c2))
+                except PP.TemplateError:
+                    continue
+                _check(m, 5, pts)
+
+
+def test_builder_bitexact_random_sets():
+    rng = np.random.default_rng(0)
+    for trial in range(3000):
+        r = int(rng.choice([2, 3, 5]))
+        n = int(rng.integers(r, 13))
+        m = n - r + 1
+        modified = bool(rng.integers(0, 2))
+        nf = n - 1 if modified else n
+        vals = list(np.unique(rng.standard_normal(nf) * rng.choice([0.1, 1.0, 10.0])))
+        if len(vals) != nf:
+            continue
+        if rng.integers(0, 3) == 0 and nf >= 3:  # symmetric pairs
+            vals[1] = -vals[0]
+            if len(set(vals)) != nf:
+                continue
+        pts = [float(v) for v in rng.permutation(vals)] + ([INF] if modified else [])
+        _check(m, r, pts)
+
+
+def test_templates_match_oracle_templates():
+    for c in synth.c_grid()[::17]:
+        assert PP.family_f43(float(c)) == OP.f43_c(float(c))
+        assert PP.family_f23(float(c)) == OP.f23_c(float(c))
+    assert PP.family_n8_cd(2.0, 1.003) == OP.n8_cd(2.0, 1.003)
+    assert PP.P8 == OP.P8 and PP.P10 == OP.P10
+
+
+@pytest.mark.parametrize("m,r,pts,status", [
+    (2, 3, [-1.0, 0.0, 1.0], 2),
+    (2, 3, [-1.0, 0.0, 0.0, INF], 3),
+    (2, 3, [-1.0, 0.0, -0.0, INF], 3),
+    (2, 3, [-1.0, INF, 1.0, 2.0], 4),
+    (2, 3, [-1.0, 0.0, 1.0, -INF], 4),
+    (2, 3, [-1.0, math.nan, 1.0, INF], 5),
+    (0, 3, [0.0, 1.0], 1),
+    (10, 8, [float(i) for i in range(17)], 8),
+])
+def test_builder_errors(m, r, pts, status):
+    with pytest.raises(_lib.WinoError) as ei:
+        api.wino_points_to_matrices(m, r, pts)
+    assert ei.value.status == status
+
+
+def test_supported_table():
+    assert api.wino_supported(2, 4, 3) and api.wino_supported(1, 4, 3)
+    assert api.wino_supported(0, 6, 3) and api.wino_supported(0, 2, 3)
+    assert not api.wino_supported(3, 4, 3)
+
+
+def test_workspace_sizes():
+    assert api.wino_error_sweep_workspace_bytes(2, 4, 3, 4096, 100_000) > 100_000 * 16 * 8
+    b = api.wino_conv2d_workspace_bytes(32, 256, 56, 56, 256, 3, 1, 6)
+    assert b > 3 * 64 * 256 * 3200 * 4 // 2
+    assert api.wino_conv2d_workspace_bytes(1, 1, 1, 1, 1, 3, 0, 2) == 0

@@ -1,0 +1,122 @@
+"""GPU parity of the fp32 Winograd layer (wino_conv2d_fp32) against the oracle's O4/O5
+layer: outputs bit-identical; scored statistics vs the oracle's fp64 direct convolution
+within the north-star tolerance (we assert 1e-9 relative on the MAE)."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import points as OP, ref
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _run(x, w, pad, m, pts, score=True):
+    import torch
+    from paper_2201_10369_b200 import api
+    y, s, mx = api.conv2d(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), pad, m, pts, score=score)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), (s.cpu().numpy() if score else None), (mx.cpu().numpy() if score else None)
+
+
+def _oracle_stats(x, w, pad, y_oracle):
+    y64 = ref.conv2d_direct64(x, w, pad)
+    return ref.stats(y_oracle, y64)
+
+
+def _check_stats(s, mx, s_ref, m_ref):
+    assert s[3] == s_ref[3] and s[4] == s_ref[4]
+    assert np.array_equal(mx, m_ref)
+    assert abs((s[0] / s[3]) / (s_ref[0] / s_ref[3]) - 1) < 1e-9
+    assert abs(s[1] / s_ref[1] - 1) < 1e-9
+
+
+def test_cfg1_full():
+    """BASELINE.json configs[0]: F(2x2,3x3), {0,-1,1,inf}, N=1 C=K=8 16x16 pad 1, U[-1,1] seed 0."""
+    x, w = synth.layer_inputs(1, 8, 16, 16, 8, 3, "uniform", "uniform", seed=0)
+    pts = OP.f23_c(1.0)
+    y, s, mx = _run(x, w, 1, 2, pts)
+    y_ref = ref.conv2d_wino(x, w, 1, 2, pts)
+    assert np.array_equal(y, y_ref)
+    s_ref, m_ref = _oracle_stats(x, w, 1, y_ref)
+    _check_stats(s, mx, s_ref, m_ref)
+    assert 0 < s_ref[0] / s_ref[3] < 1e-6
+
+
+def test_cfg1_integer_exact():
+    x, w = synth.integer_layer_inputs(1, 8, 16, 16, 8, 3, seed=0)
+    y, s, mx = _run(x, w, 1, 2, OP.f23_c(1.0))
+    y64 = ref.conv2d_direct64(x, w, 1)
+    assert np.array_equal(y.astype(np.float64), y64)
+    assert s[0] == 0.0 and mx[0] == 0.0
+
+
+@pytest.mark.parametrize("N,C,H,W,K,r,pad,m,pts", [
+    (2, 13, 19, 23, 37, 3, 1, 6, OP.n8_cd(2.0, 1.003)),      # ragged everything, cfg3 template
+    (2, 16, 20, 20, 8, 3, 1, 6, OP.P8),
+    (1, 9, 17, 17, 130, 3, 0, 4, OP.f43_c(1.622)),
+    (2, 8, 18, 18, 16, 3, 1, 2, OP.f23_c(1.0)),
+    (1, 7, 21, 21, 9, 3, 1, 3, [-1.0, 0.0, 0.5, 1.0, INF]),
+    (1, 6, 20, 20, 6, 3, 1, 5, [-2.0, -1.0, 0.0, 0.5, 1.0, 2.0, INF]),
+    (2, 10, 21, 21, 12, 5, 2, 4, OP.n8_c1c2(1.5, 3.1)),
+    (1, 10, 22, 22, 12, 5, 2, 6, OP.n10_c1c2(1.272, 2.099)),
+    (1, 3, 9, 9, 4, 5, 2, 2, [-1.0, 0.0, 1.0, 2.0, -2.0, INF][:5] + [INF]),
+])
+def test_layer_bitexact(N, C, H, W, K, r, pad, m, pts):
+    pts = sorted(p for p in pts if p != INF) + [INF]
+    x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=3)
+    y, s, mx = _run(x, w, pad, m, pts)
+    y_ref = ref.conv2d_wino(x, w, pad, m, pts)
+    assert np.array_equal(y, y_ref)
+    s_ref, m_ref = _oracle_stats(x, w, pad, y_ref)
+    _check_stats(s, mx, s_ref, m_ref)
+
+
+def test_cfg3_full_size_sampled_images():
+    """BASELINE.json configs[2] at full size (N=32, C=K=256, 56x56, F(6x6,3x3), X16 points)
+    in the bench's launch configuration; images 0 and 31 recomputed by the oracle."""
+    x, w = synth.layer_inputs(32, 256, 56, 56, 256, 3, "normal", "he", seed=0)
+    pts = OP.n8_cd(2.0, 1.003)
+    y, _, _ = _run(x, w, 1, 6, pts, score=False)
+    for img in (0, 31):
+        y_ref = ref.conv2d_wino(x, w, 1, 6, pts, n_lo=img, n_hi=img + 1)
+        assert np.array_equal(y[img], y_ref[img])
+
+
+def test_cfg3_shape_scored_two_images():
+    x, w = synth.layer_inputs(2, 256, 56, 56, 256, 3, "normal", "he", seed=0)
+    pts = OP.n8_cd(2.0, 1.003)
+    y, s, mx = _run(x, w, 1, 6, pts)
+    y_ref = ref.conv2d_wino(x, w, 1, 6, pts)
+    assert np.array_equal(y, y_ref)
+    s_ref, m_ref = _oracle_stats(x, w, 1, y_ref)
+    _check_stats(s, mx, s_ref, m_ref)
+
+
+def test_cfg4_full_size_image0():
+    """BASELINE.json configs[3] shapes: N=16, C=K=128, 64x64, 5x5, F(4x4) and F(6x6)."""
+    x, w = synth.layer_inputs(16, 128, 64, 64, 128, 5, "uniform", "uniform", seed=0)
+    for m, pts in ((4, OP.n8_c1c2(1.5, 3.1)), (6, OP.n10_c1c2(1.272, 2.099))):
+        y, _, _ = _run(x, w, 2, m, pts, score=False)
+        y_ref = ref.conv2d_wino(x, w, 2, m, pts, n_lo=0, n_hi=1)
+        assert np.array_equal(y[0], y_ref[0])
+
+
+def test_layer_errors():
+    import torch
+    from paper_2201_10369_b200 import api, _lib
+    x = torch.zeros((1, 2, 8, 8), device="cuda")
+    w = torch.zeros((2, 2, 3, 3), device="cuda")
+    y = torch.zeros((1, 2, 8, 8), device="cuda")
+    ws = torch.empty(8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(_lib.WinoError) as ei:
+        api.wino_conv2d_fp32(x, w, y, 1, 2, OP.f23_c(1.0), ws)
+    assert ei.value.status == 6
+    with pytest.raises(_lib.WinoError) as ei:
+        api.wino_conv2d_fp32(x, w, y, 1, 2, [0.0, 0.0, 1.0, INF], ws)
+    assert ei.value.status in (3, 6)
+    with pytest.raises(_lib.WinoError) as ei:
+        api.wino_conv2d_fp32(x, w, y, 1, 9, [float(i) for i in range(10)] + [INF], ws)
+    assert ei.value.status == 8
