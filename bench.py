@@ -1,0 +1,449 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path (BASELINE.json metric "Winograd conv effective TFLOP/s
+(direct-FLOP equiv) and c-sweep tiles/s at 1/2/4/8").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A STEP is the whole configs[1] job: four sweeps
+(1D / 2D F(4,3) x uniform / normal tiles) of 4096 log-spaced c over 100,000 shared random
+tiles each, every output scored against fp64 direct correlation, candidates sharded over
+the ranks, statistics all-reduced (NCCL).  `value` = tile-evaluations per second of the
+whole job (candidates x tiles, all four sweeps) -- strong scaling: the job is fixed, ranks
+split the candidates.  The configs[2] layer (a3-a7, F(6x6,3x3), N=32 C=K=256 56x56) is
+measured on rank 0 beside it and reported under "layer" (effective direct-equivalent
+TFLOP/s), unscored and scored.
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
+launching stream, the L2 flushed (512 MB write) between steps outside the events;
+barrier + synchronize around the timed region; max over ranks.  Clocks are sampled with
+NVML during the timed region.  `e2e` repeats the job through the same C-ABI call with the
+tiles copied H2D from pinned host memory and the statistics copied back D2H inside the
+timed region.  `cpu_baseline` / `--impl reference` time the oracle (oracle/, plain C,
+OpenMP) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "Winograd conv effective TFLOP/s (direct-FLOP equiv) and c-sweep tiles/s at 1/2/4/8"
+N_C = 4096
+N_TILES = 100_000
+L2_FLUSH_BYTES = 512 << 20
+
+
+# ------------------------------------------------------------------ helpers
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """NVML sampler of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int, period: float = 0.05):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self._thr = None
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, v in self.REASONS.items():
+                    if mask & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _flops_per_tile_eval(dims, m, r, AT, G, BT):
+    """Algorithmic work of one tile evaluation with the template's structural zeros skipped
+    (SURVEY §8(d)): FMAs of the canonical O5 chains whose coefficient is non-zero, plus the
+    Hadamard multiplies; FLOP = 2 FMA + MUL.  Also returns the dense FMA count."""
+    n = m + r - 1
+    nz = lambda M: int(np.count_nonzero(M))
+    if dims == 1:
+        fma = nz(G) + nz(BT) + nz(AT)
+        dense = n * r + n * n + m * n
+        mul = n
+    else:
+        fma = (r + n) * nz(G) + 2 * n * nz(BT) + (n + m) * nz(AT)
+        dense = n * r * r + n * n * r + 2 * n * n * n + m * n * n + m * m * n
+        mul = n * n
+    return 2 * fma + mul, fma, dense, mul
+
+
+# ------------------------------------------------------------------ reference arm / cpu baseline
+
+def oracle_sample_run(specs, every: int):
+    """Time the oracle (as it stands) on every `every`-th candidate of each sweep, all tiles.
+    Returns (tile_evals, seconds, threads, sample description)."""
+    from oracle import points as OP, ref
+    ref.lib()
+    threads = ref.max_threads()
+    evals = 0
+    dt = 0.0
+    for sp in specs:
+        d, g = synth.random_tiles(sp.n_tiles, sp.dims, sp.n, sp.r, sp.dist, sp.seed)
+        t0 = time.perf_counter()
+        sets = [OP.f43_c(float(c)) for c in sp.params[::every]]
+        ref.sweep(sp.dims, sp.m, sp.r, sets, d, g)
+        dt += time.perf_counter() - t0
+        evals += len(sets) * sp.n_tiles
+    desc = (f"every {every}th of {N_C} c (={len(specs[0].params[::every])} c) x {specs[0].n_tiles} tiles x "
+            f"{len(specs)} sweeps, oracle/ref.c OpenMP")
+    return evals, dt, threads, desc
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle on the host cores is the reference arm (tier framing)."""
+    if rank != 0:
+        return 0
+    from paper_2201_10369_b200.sweep import cfg2_specs
+    specs = cfg2_specs(synth.c_grid(N_C), args.n_tiles)
+    every = args.ref_every
+    for _ in range(max(0, args.warmup)):
+        oracle_sample_run(specs, every * 8)
+    times, evals, threads, desc = [], 0, 1, ""
+    for _ in range(args.steps):
+        evals, dt, threads, desc = oracle_sample_run(specs, every)
+        times.append(dt)
+    tot = sum(times)
+    value = evals * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tile-evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "configs[1] c-sweep (bounded sample per step)", "n_c": N_C, "n_tiles": args.n_tiles,
+                   "sweeps": [s.name for s in specs], "template": "{0,±c,±1/c,inf} F(4,3)"},
+        "cpu_baseline": {"value": value, "unit": "tile-evals/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "tile-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ native arm
+
+def bench_layer(torch, dev, flush, steps=10):
+    """configs[2]: F(6x6,3x3) layer, N=32 C=K=256 56x56 pad 1, X16 points; unscored + scored."""
+    from paper_2201_10369_b200 import api, points as PP
+    N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
+    x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
+    xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
+    pts = PP.family_n8_cd(2.0, 1.003)
+    Ho, Wo = H, W
+    y = torch.empty((N, K, Ho, Wo), dtype=torch.float32, device=dev)
+    ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, W, K, r, pad, m), dtype=torch.uint8, device=dev)
+    sums = torch.zeros(5, dtype=torch.float64, device=dev)
+    maxs = torch.zeros(2, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
+    torch.cuda.synchronize()
+    fams = ["layer_filter", "layer_input", "layer_gemm", "layer_output"]
+    api.wino_timing_reset()
+    api.wino_timing_enable(True)
+    ts = []
+    for _ in range(steps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    kern = {f: api.wino_timing_read(f)[0] / steps for f in fams}
+    api.wino_timing_reset()
+    # scored (fp64 direct scoring on every output)
+    sc = []
+    for _ in range(2):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sums, maxs)
+        b.record(stream)
+        b.synchronize()
+        sc.append(a.elapsed_time(b))
+    api.wino_timing_enable(False)
+    s = sums.cpu().numpy() / 2
+    t = statistics.median(ts)
+    direct_flop = 2.0 * N * K * C * Ho * Wo * r * r
+    # roofline: algorithmic FP32 work (GEMM MACs + zero-skipped transform FMAs) and fused bytes
+    AT, G, BT = api.wino_points_to_matrices(m, r, pts)
+    n = m + r - 1
+    th = tw = (Ho + m - 1) // m
+    T = N * th * tw
+    gemm_mac = n * n * K * C * T
+    nzG, nzB, nzA = (int(np.count_nonzero(M)) for M in (G, BT, AT))
+    tr_fma = K * C * (r + n) * nzG + C * T * 2 * n * nzB + K * T * (n + m) * nzA
+    f_alg = 2.0 * (gemm_mac + tr_fma)
+    b_alg = 4.0 * (x.size + w.size + N * K * Ho * Wo)
+    return {
+        "workload": "configs[2] F(6x6,3x3) N=32 C=K=256 56x56 pad 1, points {0,±2,±1/2,-1/1.003,1.003,inf}",
+        "ms": t, "ms_min": min(ts), "effective_tflops": direct_flop / (t * 1e-3) / 1e12,
+        "kernel_ms": kern, "flop_alg": f_alg, "bytes_alg": b_alg,
+        "scored_ms": statistics.median(sc), "scored_mae": float(s[0] / s[3]) if s[3] else None,
+        "l2": "flushed (512 MB write) before every run",
+    }, f_alg, b_alg, t
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--n-tiles", type=int, default=N_TILES)
+    ap.add_argument("--ref-every", type=int, default=32, help="oracle sample: every k-th candidate")
+    ap.add_argument("--no-layer", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2201_10369_b200 import api
+    from paper_2201_10369_b200.sweep import cfg2_specs, make_rank_sweep, run_step
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    api.wino_supported(2, 4, 3)  # loads libwino.so (fails loudly if missing)
+
+    specs = cfg2_specs(synth.c_grid(N_C), args.n_tiles)
+    host = []
+    rsw = []
+    for sp in specs:
+        d, g = synth.random_tiles(sp.n_tiles, sp.dims, sp.n, sp.r, sp.dist, sp.seed)
+        host.append((d, g))
+        rsw.append(make_rank_sweep(sp, rank, world, dev, d, g))
+    stream = torch.cuda.current_stream()
+    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        flush_buf.zero_()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        run_step(rsw)
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    api.wino_timing_reset()
+    api.wino_timing_enable(True)
+    step_ms = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            launches += run_step(rsw)
+            b.record(stream)
+            step_ms.append((a, b))
+        torch.cuda.synchronize()
+        barrier()
+    api.wino_timing_enable(False)
+    step_ms = [a.elapsed_time(b) for a, b in step_ms]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    evals_per_step = sum(sp.n_cand * sp.n_tiles for sp in specs)
+    value = evals_per_step * args.steps / (tot_ms * 1e-3)
+
+    # dominant kernel (2D sweep) live timing -> roofline
+    k2_ms, k2_n = api.wino_timing_read("sweep2d")
+    k1_ms, _ = api.wino_timing_read("sweep1d")
+    kref_ms, _ = api.wino_timing_read("sweep_refs2d")
+    kfin_ms, _ = api.wino_timing_read("sweep_finalize")
+    api.wino_timing_reset()
+    sp2 = specs[2]
+    AT, G, BT = api.wino_points_to_matrices(4, 3, sp2.point_sets(100, 101)[0])
+    flop_te, fma_te, dense_te, mul_te = _flops_per_tile_eval(2, 4, 3, AT, G, BT)
+    evals_2d = sum(rs.hi - rs.lo for rs in rsw if rs.spec.dims == 2) * sp2.n_tiles * args.steps
+    peaks, peak_src = _peaks()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = nsm * 128 * 2 * fmax * 1e6 / 1e12
+    achieved = evals_2d * flop_te / (k2_ms * 1e-3) / 1e12 if k2_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("sweep2d_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "kernel": "sweep2d_kernel<4,3> (K7, 2D F(4x4,3x3))", "bound": "alu", "achieved": achieved,
+        "peak": fp32_peak, "unit": "TFLOP/s", "frac": (achieved / fp32_peak) if achieved else None,
+        "traffic": traffic,
+        "peak_source": f"FP32 FFMA: {nsm} SMs x 128 lanes x 2 FLOP x {fmax:.0f} MHz (sm_max_mhz, {peak_src}); "
+                       "microbench profiles/r01_pipes_microbench.jsonl measured 7.2e13",
+        "flop_per_tile_eval": flop_te, "fma_per_tile_eval_zero_skipped": fma_te, "fma_per_tile_eval_dense": dense_te,
+        "mul_per_tile_eval": mul_te, "kernel_ms_total": k2_ms, "launches": k2_n,
+        "avg_launch_ms": k2_ms / k2_n if k2_n else None,
+        "share_of_step": k2_ms / sum(step_ms) if step_ms else None,
+        "other_kernels_ms": {"sweep1d": k1_ms, "sweep_refs2d": kref_ms, "sweep_finalize": kfin_ms},
+    }
+
+    # ---- e2e: same job through the C-ABI with host tiles, H2D + D2H inside the timed region
+    pinned = [(torch.from_numpy(d).pin_memory(), torch.from_numpy(g).pin_memory()) for d, g in host]
+    out_host = [(torch.empty(rs.sums.shape, dtype=torch.float64).pin_memory(),
+                 torch.empty(rs.maxs.shape, dtype=torch.float64).pin_memory()) for rs in rsw]
+    h2d = sum(p[0].numel() * 4 + p[1].numel() * 4 for p in pinned)
+    d2h = sum(o[0].numel() * 8 + o[1].numel() * 8 for o in out_host)
+    e2e_ms = []
+    barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for rs, (pd, pg) in zip(rsw, pinned):
+            rs.d_tiles.copy_(pd, non_blocking=True)
+            rs.g_tiles.copy_(pg, non_blocking=True)
+        run_step(rsw)
+        for rs, (hs, hm) in zip(rsw, out_host):
+            hs.copy_(rs.sums, non_blocking=True)
+            hm.copy_(rs.maxs, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_tot = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_value = evals_per_step * args.steps / (e2e_tot * 1e-3)
+
+    # results of the job (rank 0 holds the reduced curve)
+    from paper_2201_10369_b200.sweep import argmin_c, curve
+    results = {}
+    for rs in rsw:
+        mae = curve(out_host[rsw.index(rs)][0].numpy())
+        i, best = argmin_c(rs.spec.params, mae)
+        results[rs.spec.name] = {"argmin_c": float(rs.spec.params[i]) if i is not None else None,
+                                 "min_mae": best, "n_nonfinite_candidates": int(np.sum(~np.isfinite(mae)))}
+
+    layer = None
+    if rank == 0 and world == 1 and not args.no_layer:
+        layer, f_alg, b_alg, t_layer = bench_layer(torch, dev, flush)
+        t_roof = max(f_alg / (fp32_peak * 1e12), b_alg / (float(peaks.get("hbm_gbs", 6458.7)) * 1e9))
+        layer["roofline_frac"] = t_roof / (t_layer * 1e-3)
+        layer["roofline_bound"] = "fp32 FFMA (t_roof = max(F_alg/P_fp32, B_alg/BW_hbm))"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        evals_c, dt_c, thr, desc = oracle_sample_run(specs, args.ref_every)
+        cpu = {"value": evals_c / dt_c, "unit": "tile-evals/s", "cores": thr, "kind": "oracle", "sample": desc,
+               "seconds": dt_c}
+
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tile-evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "configs[1]: c-sweep F(4,3) 1D + F(4x4,3x3) 2D, {0,±c,±1/c,inf}, "
+                                   f"{N_C} log-spaced c in [0.05,20], {args.n_tiles} tiles/sweep, "
+                                   "uniform[-1,1] + N(0,1), scored vs fp64 direct",
+                       "tile_evals_per_step": evals_per_step, "parallelism": f"candidates/{world} ranks",
+                       "l2": "flushed (512 MB write) between timed steps; step inputs 46 MB < L2"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "tile-evals/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "step_ms": step_ms,
+            "results": results,
+            "layer": layer,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

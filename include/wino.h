@@ -45,8 +45,10 @@ typedef enum {
  * and a normal convolution using double precision"; per element, reading R10).  fp64,
  * per scored unit (candidate, or layer):
  *   sums[5] = { Σ|e|, Σe², Σ|y_ref|, n_scored, n_nonfinite },  maxs[2] = { max|e|, max|y_ref| }
- * with e = RN64((double)y32 − y64) for every output; non-finite e only increments
- * n_nonfinite.  Calls ACCUMULATE (sums +=, maxs = max) so buffers can be summed over
+ * with e = RN64((double)y32 − y64) for every output.  A non-finite e only increments
+ * n_nonfinite (it is excluded from Σ|e|, Σe², max|e|, n_scored); Σ|y_ref| and max|y_ref|
+ * describe the reference and run over every output (reading R16).
+ * Calls ACCUMULATE (sums +=, maxs = max) so buffers can be summed over
  * calls and all-reduced over ranks; the caller zero-initialises them.
  * Mean absolute error = sums[0] / sums[3]. */
 #define WINO_SUMS 5
@@ -125,6 +127,17 @@ int wino_sweep_outputs(int dims, int m, int r, const double* point_sets, int n_c
 /* Number of kernel launches the last successful call on this thread enqueued
  * (for bench.py's gpu_launches count). */
 int wino_last_launch_count(void);
+
+/* Kernel timing hook (profiling / bench.py roofline).  While enabled, every launch is
+ * bracketed by two cudaEvents recorded on its own stream and filed under its kernel
+ * family: "sweep1d", "sweep2d", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
+ * "layer_filter", "layer_input", "layer_gemm", "layer_output", "layer_score",
+ * "layer_score_finalize".  wino_timing_read() synchronises on the recorded events and
+ * returns the summed milliseconds and launch count of one family since the last reset.
+ * Returns the previous enable state / a wino_status. */
+int wino_timing_enable(int enable);
+void wino_timing_reset(void);
+int wino_timing_read(const char* family, double* total_ms, int* launches);
 
 #ifdef __cplusplus
 }

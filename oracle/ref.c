@@ -159,17 +159,20 @@ static void direct32_tile(int dims, int m, int r, const float* d, const float* g
   }
 }
 
-/* O8: e = RN64((double)y32 - y64); non-finite e counted and excluded. */
+/* O8: e = RN64((double)y32 - y64).  A non-finite e is counted (n_nonfinite) and excluded
+ * from Σ|e|, Σe², max|e| and n_scored; Σ|y_ref| and max|y_ref| describe the reference and
+ * run over every output (reading R16). */
 static inline void stat_acc(double* sums, double* maxs, float y32, double y64) {
   double e = (double)y32 - y64;
+  double ay = fabs(y64);
+  sums[2] += ay;
+  if (ay > maxs[1]) maxs[1] = ay;
   if (!isfinite(e)) { sums[4] += 1.0; return; }
-  double ae = fabs(e), ay = fabs(y64);
+  double ae = fabs(e);
   sums[0] += ae;
   sums[1] += e * e;
-  sums[2] += ay;
   sums[3] += 1.0;
   if (ae > maxs[0]) maxs[0] = ae;
-  if (ay > maxs[1]) maxs[1] = ay;
 }
 
 /* ---------------------------------------------------------------- exported API */

@@ -33,6 +33,9 @@ SIGNATURES = [
     ("wino_sweep_outputs", ctypes.c_int,
      [ctypes.c_int] * 3 + [_d, ctypes.c_int, _vp, _vp, _i64, _vp, _i, ctypes.c_uint, _vp]),
     ("wino_last_launch_count", ctypes.c_int, []),
+    ("wino_timing_enable", ctypes.c_int, [ctypes.c_int]),
+    ("wino_timing_reset", None, []),
+    ("wino_timing_read", ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), _i]),
 ]
 
 _lib = None

@@ -116,6 +116,21 @@ def wino_last_launch_count() -> int:
     return int(load().wino_last_launch_count())
 
 
+def wino_timing_enable(enable: bool) -> bool:
+    return bool(load().wino_timing_enable(int(enable)))
+
+
+def wino_timing_reset() -> None:
+    load().wino_timing_reset()
+
+
+def wino_timing_read(family: str) -> Tuple[float, int]:
+    ms = ctypes.c_double(0.0)
+    n = ctypes.c_int(0)
+    check(load().wino_timing_read(family.encode(), ctypes.byref(ms), ctypes.byref(n)), "wino_timing_read")
+    return ms.value, n.value
+
+
 # ------------------------------------------------------------------ convenience (still marshalling only)
 
 def conv2d(x, w, pad: int, m: int, points, score: bool = False, stream=None):

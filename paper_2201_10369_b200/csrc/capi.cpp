@@ -1,5 +1,7 @@
 // The C ABI of libwino (include/wino.h): validation, host matrix construction, launch.
 #include <cmath>
+#include <mutex>
+#include <string>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -24,6 +26,34 @@ int set_error(int status, const char* fmt, ...) {
 }
 void count_launches(int n) { g_launches += n; }
 void reset_launches() { g_launches = 0; }
+
+namespace {
+struct Rec {
+  std::string family;
+  cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+}  // namespace
+
+bool timing_enabled() { return g_timing; }
+cudaEvent_t timing_event() {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+void timing_record(const char* family, cudaEvent_t a, cudaEvent_t b) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_recs.push_back(Rec{family, a, b});
+}
 
 }  // namespace wino
 
@@ -61,6 +91,41 @@ const char* wino_status_string(int status) {
 const char* wino_last_error(void) { return g_err; }
 
 int wino_last_launch_count(void) { return g_last_launches; }
+
+int wino_timing_enable(int enable) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  const int prev = g_timing ? 1 : 0;
+  g_timing = enable != 0;
+  return prev;
+}
+
+void wino_timing_reset(void) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (auto& r : g_recs) {
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_recs.clear();
+}
+
+int wino_timing_read(const char* family, double* total_ms, int* launches) {
+  if (!family || !total_ms || !launches) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  std::lock_guard<std::mutex> lk(g_tmu);
+  double tot = 0.0;
+  int cnt = 0;
+  for (auto& r : g_recs) {
+    if (r.family != family) continue;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaEventSynchronize: %s", cudaGetErrorString(e));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    tot += ms;
+    cnt++;
+  }
+  *total_ms = tot;
+  *launches = cnt;
+  return WINO_OK;
+}
 
 int wino_supported(int dims, int m, int r) {
   if (dims == 1 || dims == 2) return sweep_supported(dims, m, r);
@@ -123,23 +188,8 @@ static int sweep_common(int dims, int m, int r, const double* point_sets, int n_
   if (n > WINO_MAX_N) return set_error(WINO_E_UNSUPPORTED, "n > WINO_MAX_N");
   if (!sweep_supported(dims, m, r))
     return set_error(WINO_E_UNSUPPORTED, "no sweep kernel for dims=%d m=%d r=%d", dims, m, r);
-  const int per = m * n + n * r + n * n;
-  std::vector<float> mats((size_t)(n_cand > 0 ? n_cand : 1) * per);
-  std::vector<int> ok(n_cand > 0 ? n_cand : 1);
-  std::vector<double> AT(m * n), G(n * r), BT(n * n);
-  for (int c = 0; c < n_cand; c++) {
-    const int s = build_r64(m, r, point_sets + (size_t)c * n, n, AT.data(), G.data(), BT.data());
-    cand_status[c] = s;
-    ok[c] = s == WINO_OK;
-    if (s == WINO_OK) {
-      float* dst = mats.data() + (size_t)c * per;
-      to_f32(AT.data(), m * n, dst);
-      to_f32(G.data(), n * r, dst + m * n);
-      to_f32(BT.data(), n * n, dst + m * n + n * r);
-    }
-  }
-  return finish(sweep_launch(dims, m, r, mats.data(), ok.data(), n_cand, d_tiles, g_tiles, n_tiles, d_sums, d_maxs,
-                             d_y, workspace, ws_bytes, flags, (cudaStream_t)stream));
+  return finish(sweep_launch(dims, m, r, point_sets, cand_status, n_cand, d_tiles, g_tiles, n_tiles, d_sums,
+                             d_maxs, d_y, workspace, ws_bytes, flags, (cudaStream_t)stream));
 }
 
 int wino_error_sweep(int dims, int m, int r, const double* point_sets, int n_cand, const float* d_tiles,

@@ -15,7 +15,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
-#include <vector>
 
 #include "wino_internal.h"
 
@@ -23,49 +22,62 @@ namespace wino {
 
 namespace {
 
-// Ascending coefficients of ∏_{s in S}(x − s) (length |S| + 1).
-void root_product(const std::vector<double>& S, std::vector<double>& p) {
-  bool has_zero = false;
-  std::vector<double> nz;
-  for (double s : S) {
-    if (s == 0.0) has_zero = true;
-    else nz.push_back(s);
-  }
-  std::vector<double> pos;
-  for (double a : nz)
-    if (a > 0.0 && std::find(nz.begin(), nz.end(), -a) != nz.end()) pos.push_back(a);
-  std::sort(pos.begin(), pos.end());
-  std::vector<double> lin;
-  for (double x : nz) {
-    const double ax = std::fabs(x);
-    if (!std::binary_search(pos.begin(), pos.end(), ax)) lin.push_back(x);
-  }
-  std::sort(lin.begin(), lin.end());
+constexpr int kCap = WINO_MAX_N + 2;
 
-  p.assign(1, 1.0);
-  std::vector<double> q;
-  for (double a : pos) {
-    const double s = a * a;
-    const int L = (int)p.size();
-    q.assign(L + 2, 0.0);
+// Ascending coefficients of ∏_{s in S}(x − s); returns the length |S| + 1.
+// Fixed-size arrays: no allocation per candidate (this runs for every candidate of a sweep).
+int root_product(const double* S, int ns, double* p) {
+  bool has_zero = false;
+  double nz[kCap], pos[kCap], lin[kCap];
+  int nnz = 0, npos = 0, nlin = 0;
+  for (int i = 0; i < ns; i++) {
+    if (S[i] == 0.0) has_zero = true;
+    else nz[nnz++] = S[i];
+  }
+  for (int i = 0; i < nnz; i++) {
+    if (!(nz[i] > 0.0)) continue;
+    for (int j = 0; j < nnz; j++)
+      if (nz[j] == -nz[i]) {
+        pos[npos++] = nz[i];
+        break;
+      }
+  }
+  std::sort(pos, pos + npos);
+  for (int i = 0; i < nnz; i++) {
+    const double ax = std::fabs(nz[i]);
+    if (!std::binary_search(pos, pos + npos, ax)) lin[nlin++] = nz[i];
+  }
+  std::sort(lin, lin + nlin);
+
+  double q[kCap];
+  int L = 1;
+  p[0] = 1.0;
+  for (int t = 0; t < npos; t++) {
+    const double s = pos[t] * pos[t];
     for (int j = 0; j < L + 2; j++) {
       const double pj2 = (j - 2 >= 0 && j - 2 < L) ? p[j - 2] : 0.0;
       const double pj = (j < L) ? p[j] : 0.0;
       q[j] = pj2 - s * pj;
     }
-    p.swap(q);
+    L += 2;
+    std::copy(q, q + L, p);
   }
-  for (double r : lin) {
-    const int L = (int)p.size();
-    q.assign(L + 1, 0.0);
+  for (int t = 0; t < nlin; t++) {
+    const double r = lin[t];
     for (int j = 0; j < L + 1; j++) {
       const double pj1 = (j - 1 >= 0 && j - 1 < L) ? p[j - 1] : 0.0;
       const double pj = (j < L) ? p[j] : 0.0;
       q[j] = pj1 - r * pj;
     }
-    p.swap(q);
+    L += 1;
+    std::copy(q, q + L, p);
   }
-  if (has_zero) p.insert(p.begin(), 0.0);
+  if (has_zero) {
+    for (int j = L; j > 0; j--) p[j] = p[j - 1];
+    p[0] = 0.0;
+    L += 1;
+  }
+  return L;
 }
 
 }  // namespace
@@ -99,9 +111,8 @@ int build_r64(int m, int r, const double* pts, int n, double* AT, double* G, dou
   std::memset(AT, 0, sizeof(double) * m * n);
   std::memset(G, 0, sizeof(double) * n * r);
   std::memset(BT, 0, sizeof(double) * n * n);
-  std::vector<double> S, p;
+  double S[kCap], p[kCap], pw[kCap];
   const int npw = std::max(m, r);
-  std::vector<double> pw(npw);
   for (int i = 0; i < nf; i++) {
     const double a = pts[i];
     double Ni = 1.0;
@@ -111,18 +122,17 @@ int build_r64(int m, int r, const double* pts, int n, double* AT, double* G, dou
     for (int t = 1; t < npw; t++) pw[t] = pw[t - 1] * a;
     for (int t = 0; t < m; t++) AT[t * n + i] = pw[t];
     for (int q = 0; q < r; q++) G[i * r + q] = pw[q] / Ni;
-    S.clear();
+    int ns = 0;
     for (int j = 0; j < nf; j++)
-      if (j != i) S.push_back(pts[j]);
-    root_product(S, p);
-    for (size_t j = 0; j < p.size(); j++) BT[i * n + j] = p[j];
+      if (j != i) S[ns++] = pts[j];
+    const int L = root_product(S, ns, p);
+    for (int j = 0; j < L; j++) BT[i * n + j] = p[j];
   }
   if (has_inf) {
     AT[(m - 1) * n + nf] = 1.0;
     G[nf * r + (r - 1)] = 1.0;
-    S.assign(pts, pts + nf);
-    root_product(S, p);
-    for (size_t j = 0; j < p.size(); j++) BT[nf * n + j] = p[j];
+    const int L = root_product(pts, nf, p);
+    for (int j = 0; j < L; j++) BT[nf * n + j] = p[j];
   }
   return WINO_OK;
 }

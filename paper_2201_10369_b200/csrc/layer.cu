@@ -309,12 +309,12 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(const float* __res
       }
     }
     const double e = (double)y[o] - acc;
+    st.s2 += fabs(acc);
+    st.m1 = fmax(st.m1, fabs(acc));
     if (isfinite(e)) {
       st.s0 += fabs(e);
       st.s1 = __fma_rn(e, e, st.s1);
-      st.s2 += fabs(acc);
       st.m0 = fmax(st.m0, fabs(e));
-      st.m1 = fmax(st.m1, fabs(acc));
       st.n++;
     } else {
       st.nonfin++;
@@ -437,27 +437,34 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   int launches = 0;
   {
     const long long tot = (long long)g.Cp * g.Kp;
-    cfg->fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(w, U, C, K, g.Cp, g.Kp, mt);
+    const auto fk = cfg->fk;
+    timed_launch("layer_filter", stream,
+                 [&] { fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(w, U, C, K, g.Cp, g.Kp, mt); });
     launches++;
   }
   {
     const long long tot = (long long)g.Cp * g.Tp;
-    cfg->ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt);
+    const auto ik = cfg->ik;
+    timed_launch("layer_input", stream, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt); });
     launches++;
   }
   {
     dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
-    gemm_kernel<<<grid, 256, 0, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+    timed_launch("layer_gemm", stream, [&] { gemm_kernel<<<grid, 256, 0, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
     launches++;
   }
   {
     const long long tot = (long long)g.K * g.T;
-    cfg->ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt);
+    const auto ok = cfg->ok;
+    timed_launch("layer_output", stream, [&] { ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt); });
     launches++;
   }
   if (d_sums) {
-    score_kernel<<<kScoreBlocks, kScoreThreads, 0, stream>>>(x, w, y, g, partial);
-    score_finalize_kernel<<<1, 32, 0, stream>>>(partial, kScoreBlocks * (kScoreThreads / 32), d_sums, d_maxs);
+    timed_launch("layer_score", stream,
+                 [&] { score_kernel<<<kScoreBlocks, kScoreThreads, 0, stream>>>(x, w, y, g, partial); });
+    timed_launch("layer_score_finalize", stream, [&] {
+      score_finalize_kernel<<<1, 32, 0, stream>>>(partial, kScoreBlocks * (kScoreThreads / 32), d_sums, d_maxs);
+    });
     launches += 2;
   }
   count_launches(launches);

@@ -1,504 +1,116 @@
 // Error sweep over candidate point sets (PAPER.md P:465 error protocol, P:472 sweep),
 // sm_100a.  Kernels:
-//   K6 sweep_refs    : y64 = fp64 direct valid correlation of every tile (c-independent, once)
-//   K7 sweep1d/2d    : per (candidate, tile) fp32 Winograd, fused in registers, scored
-//                      against y64; per-warp partial statistics
-//   K8 sweep_finalize: fixed-order reduction of the partials, accumulated into d_sums/d_maxs
+//   K6  sweep_refs      : y64 = fp64 direct valid correlation of every tile (c-independent,
+//                         once per call) + per-block Σ|y64| / max|y64|
+//   K6b sweep_refs_total: fixed-order total of those per-block reference statistics
+//   K7  sweep1d / 2d    : per (candidate, tile) fp32 Winograd, fused in registers, scored
+//                         against y64; per-(candidate, tile-group) partial statistics
+//   K8  sweep_finalize  : fixed-order reduction of the partials, accumulated into d_sums/d_maxs
 //
 // Design:
-//  * Each thread owns TWO tiles and evaluates them as a pair with FFMA2
-//    (fma.rn.f32x2): both halves use the same warp-uniform coefficient, which the
-//    hardware broadcasts from a uniform register (SASS `FFMA2 R, R.F32x2, UR.F32, R`).
-//    One FFMA2 issue = 64 lane-FMAs, so the FP32 pipe saturates at half the issue
-//    slots, leaving the other half for the fp64 scoring (separate FP64 pipe), the
-//    uniform coefficient loads and shared-memory traffic.
-//  * Coefficients of up to ~8000/per candidates ride in the kernel parameter space
-//    (__grid_constant__, 32 KB); indexing it with the warp-uniform candidate index
-//    compiles to LDCU UR, c[0x0][UR+off].
-//  * Tiles (and their y64) are staged once per CTA in shared memory and reused for
-//    every candidate of the CTA's candidate group.
-//  * Arithmetic is the canonical O5 order: every dot product is an
-//    fmaf chain from +0 in ascending index order, 2D left product first, so outputs
-//    are bit-identical to the oracle.  Rows of V are streamed: for each row i the
-//    kernel forms T1 row i -> U row i, T2 row i -> V row i, M row i = U⊙V and
-//    accumulates T3 += Aᵀ[:,i] M[i,:] -- per element the same chain as the oracle.
-#include <algorithm>
-#include <cstdio>
-#include <vector>
-
-#include "wino_internal.h"
+//  * Each thread owns TWO tiles and evaluates them as a pair with FFMA2 (fma.rn.f32x2):
+//    both halves use the same warp-uniform coefficient, broadcast from a uniform register
+//    (SASS `FFMA2 R, R.F32x2, UR.F32, R`).  One FFMA2 issue = 64 lane-FMAs, so the FP32
+//    pipe saturates at half the issue slots; the other half carries the fp64 scoring (its
+//    own FP64 pipe), the uniform coefficient loads and the shared-memory traffic.
+//  * Coefficients of up to kParamFloats/per candidates ride in the kernel parameter space
+//    (__grid_constant__); indexing it with the warp-uniform candidate index compiles to
+//    LDCU UR, c[0x0][UR+off].  The host builds chunk k+1's matrices while chunk k runs.
+//  * Structural zeros: a kernel instantiated with zero masks (ZA, ZG, ZB) skips those
+//    terms at compile time; the launcher uses it only when every candidate of the chunk
+//    is exactly zero there (e.g. the {0, ±c, ±1/c, ∞} family: 570 of 834 FMAs remain).
+//    Skipping an exactly-zero term leaves an fmaf chain bit-identical (up to a zero's sign).
+//  * A CTA owns a group of candidates and a range of tile blocks: tiles (and their y64)
+//    are staged in shared memory once per block and reused by every candidate of the
+//    group; per-candidate statistics accumulate in shared memory in tile-block order, so
+//    the partials are few and the reduction order is fixed (bitwise deterministic).
+//  * Arithmetic is the canonical O5 order: every dot product is an fmaf
+//    chain from +0 in ascending index order, 2D left product first, so outputs are
+//    bit-identical to the oracle.  Rows of V are streamed: for each row i the kernel forms
+//    T1 row i -> U row i, T2 row i -> V row i, Mw row i = U⊙V and accumulates
+//    T3 += Aᵀ[:,i] Mw[i,:] -- per element the same chain as the oracle.
+//  * Scoring: e = (double)y32 − y64; Σ|e|, Σe², max|e| per output (7 instructions).  A
+//    non-finite e makes Σ|e| non-finite; such a warp re-evaluates the candidate with
+//    per-output checks (the rare degenerate-candidate path).  Σ|y64|, max|y64| do not
+//    depend on the candidate and come from K6 (statistics layout, include/wino.h).
+#include "sweep_kernels.cuh"
 
 namespace wino {
 
-typedef unsigned long long u64;
-
-constexpr int kSwThreads = 128;        // 4 warps, one per SM sub-partition
-constexpr int kParamFloats = 7424;     // coefficient floats per launch (29696 B)
-constexpr int kMaxCandsLaunch = 512;   // + 2 KB of candidate indices: < 32764 B of params
-
-struct MatsParam {
-  float v[kParamFloats];
-};
-struct IdxParam {
-  int idx[kMaxCandsLaunch];
-};
-
-struct SweepArgs {
-  const float* d;
-  const float* g;
-  const double* y64;
-  float* ydump;
-  double* partial;     // [n_cand_launch][n_tblk][4 warps][8]
-  long long n_tiles;
-  int n_cand;          // candidates in this launch
-  int cands_per_cta;
-  int n_tblk;
-  int ydump_cand0;     // not used for indexing: dump rows are addressed by dump_idx
-};
-
-// ------------------------------------------------------------------ lane arithmetic
-// Pair<true>: two tiles per thread (FFMA2), Pair<false>: one tile (FFMA).
-// NOFMA (paper arithmetic) uses scalar __fmul_rn/__fadd_rn: ptxas 12.9 contracts
-// mul.rn.f32x2 + add.rn.f32x2 into FFMA2, so the pair form cannot express it.
-template <bool PAIR, bool NOFMA>
-struct Lane;
-
-template <bool NOFMA>
-struct Lane<true, NOFMA> {
-  typedef u64 T;
-  static constexpr int W = 2;
-  static __device__ __forceinline__ T pack(float a, float b) {
-    T p;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
-    return p;
+// ------------------------------------------------------------------ K6b
+__global__ void sweep_refs_total_kernel(const double* __restrict__ ref_part, int n_blocks, double* __restrict__ tot) {
+  const int lane = threadIdx.x;
+  double s = 0.0, mx = 0.0;
+  for (int b = lane; b < n_blocks; b += 32) {
+    s += ref_part[b * 2];
+    mx = fmax(mx, ref_part[b * 2 + 1]);
   }
-  static __device__ __forceinline__ float lo(T p) {
-    float a, b;
-    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
-    return a;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  static __device__ __forceinline__ float hi(T p) {
-    float a, b;
-    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
-    return b;
-  }
-  static __device__ __forceinline__ T zero() { return 0ull; }
-  // acc + a * c  (c broadcast to both halves)
-  static __device__ __forceinline__ T fma(T a, float c, T acc) {
-    if (NOFMA) {
-      return pack(__fadd_rn(lo(acc), __fmul_rn(lo(a), c)), __fadd_rn(hi(acc), __fmul_rn(hi(a), c)));
-    } else {
-      T d;
-      T cc = pack(c, c);
-      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(cc), "l"(acc));
-      return d;
-    }
-  }
-  // elementwise a * b + (+0): the Hadamard product of the C = 1 contraction (O5)
-  static __device__ __forceinline__ T mul(T a, T b) {
-    if (NOFMA) {
-      return pack(__fadd_rn(0.0f, __fmul_rn(lo(a), lo(b))), __fadd_rn(0.0f, __fmul_rn(hi(a), hi(b))));
-    } else {
-      T d;
-      T z = 0ull;
-      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(z));
-      return d;
-    }
-  }
-  static __device__ __forceinline__ float get(T v, int h) { return h ? hi(v) : lo(v); }
-};
-
-template <bool NOFMA>
-struct Lane<false, NOFMA> {
-  typedef float T;
-  static constexpr int W = 1;
-  static __device__ __forceinline__ T zero() { return 0.0f; }
-  static __device__ __forceinline__ T fma(T a, float c, T acc) {
-    return NOFMA ? __fadd_rn(acc, __fmul_rn(a, c)) : __fmaf_rn(a, c, acc);
-  }
-  static __device__ __forceinline__ T mul(T a, T b) {
-    return NOFMA ? __fadd_rn(0.0f, __fmul_rn(a, b)) : __fmaf_rn(a, b, 0.0f);
-  }
-  static __device__ __forceinline__ float get(T v, int) { return v; }
-};
-
-// ------------------------------------------------------------------ statistics
-struct Stat {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, m0 = 0.0, m1 = 0.0;
-  int nonfin = 0;
-  __device__ __forceinline__ void add(float y32, double y64) {
-    const double e = (double)y32 - y64;
-    if (isfinite(e)) {
-      const double ae = fabs(e), ay = fabs(y64);
-      s0 += ae;
-      s1 = __fma_rn(e, e, s1);
-      s2 += ay;
-      m0 = fmax(m0, ae);
-      m1 = fmax(m1, ay);
-    } else {
-      nonfin++;
-    }
-  }
-  // butterfly over the warp (fixed order -> deterministic)
-  __device__ __forceinline__ void warp_reduce() {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-      m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-    }
-    nonfin = __reduce_add_sync(0xffffffffu, nonfin);
-  }
-};
-
-// Write the warp partial: {s0, s1, s2, n_scored, n_nonfinite, m0, m1, 0}
-__device__ __forceinline__ void write_partial(double* p, const Stat& st, int n_valid_out) {
-  p[0] = st.s0;
-  p[1] = st.s1;
-  p[2] = st.s2;
-  p[3] = (double)(n_valid_out - st.nonfin);
-  p[4] = (double)st.nonfin;
-  p[5] = st.m0;
-  p[6] = st.m1;
-  p[7] = 0.0;
-}
-
-// ------------------------------------------------------------------ K6: fp64 references
-template <int DIMS, int M, int R>
-__global__ void sweep_refs_kernel(const float* __restrict__ d, const float* __restrict__ g,
-                                  double* __restrict__ y64, long long n_tiles) {
-  constexpr int N = M + R - 1;
-  constexpr int DN = DIMS == 1 ? N : N * N, DG = DIMS == 1 ? R : R * R, DY = DIMS == 1 ? M : M * M;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  const float* dt = d + t * DN;
-  const float* gt = g + t * DG;
-  double* yt = y64 + t * DY;
-  if (DIMS == 1) {
-    for (int p = 0; p < M; p++) {
-      double acc = 0.0;
-      for (int j = 0; j < R; j++) acc = __dadd_rn(acc, __dmul_rn((double)gt[j], (double)dt[p + j]));
-      yt[p] = acc;
-    }
-  } else {
-    for (int p = 0; p < M; p++)
-      for (int s = 0; s < M; s++) {
-        double acc = 0.0;
-        for (int u = 0; u < R; u++)
-          for (int v = 0; v < R; v++)
-            acc = __dadd_rn(acc, __dmul_rn((double)gt[u * R + v], (double)dt[(p + u) * N + s + v]));
-        yt[p * M + s] = acc;
-      }
-  }
-}
-
-// ------------------------------------------------------------------ K7 (2D)
-// smem: sd [NN][128] T (tiles), st2 [NN][128] T (T2 staging), sy [MM][W][128] double
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP>
-__global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
-                                                             const __grid_constant__ IdxParam DI) {
-  using L = Lane<PAIR, NOFMA>;
-  using T = typename L::T;
-  constexpr int W = L::W;
-  constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
-  constexpr int OFF_G = M * N, OFF_B = M * N + N * R, PER = OFF_B + N * N;
-  constexpr int TPB = kSwThreads * W;
-
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* sd = reinterpret_cast<T*>(smem);
-  T* st2 = sd + NN * kSwThreads;
-  double* sy = reinterpret_cast<double*>(st2 + NN * kSwThreads);
-
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const long long tile0 = (long long)blockIdx.x * TPB;
-  const long long ntl = a.n_tiles - tile0 < TPB ? a.n_tiles - tile0 : TPB;  // tiles in this block
-
-  // ---- stage the block's tiles (coalesced: the block's tiles are contiguous in memory)
-  {
-    float* sdf = reinterpret_cast<float*>(sd);
-    const float* src = a.d + tile0 * NN;
-    for (int idx = tid; idx < TPB * NN; idx += kSwThreads) {
-      const int tl = idx / NN, e = idx - tl * NN;
-      const float v = tl < ntl ? src[idx] : 0.0f;
-      sdf[(e * kSwThreads + (tl % kSwThreads)) * W + tl / kSwThreads] = v;
-    }
-    if (!DUMP) {
-      const double* ysrc = a.y64 + tile0 * MM;
-      for (int idx = tid; idx < TPB * MM; idx += kSwThreads) {
-        const int tl = idx / MM, o = idx - tl * MM;
-        sy[(o * W + tl / kSwThreads) * kSwThreads + (tl % kSwThreads)] = tl < ntl ? ysrc[idx] : 0.0;
-      }
-    }
-  }
-  // ---- this thread's kernel tiles g (registers)
-  T g[RR];
-#pragma unroll
-  for (int e = 0; e < RR; e++) {
-    float gv[2] = {0.0f, 0.0f};
-#pragma unroll
-    for (int h = 0; h < W; h++) {
-      const long long t = tile0 + tid + h * kSwThreads;
-      if (t < a.n_tiles) gv[h] = a.g[t * RR + e];
-    }
-    if constexpr (PAIR) g[e] = L::pack(gv[0], gv[1]);
-    else g[e] = gv[0];
-  }
-  int n_valid_out = 0;
-#pragma unroll
-  for (int h = 0; h < W; h++) n_valid_out += (tile0 + tid + h * kSwThreads < a.n_tiles) ? MM : 0;
-  {
-    // warp-level count of valid outputs (for n_scored)
-    n_valid_out = __reduce_add_sync(0xffffffffu, n_valid_out);
-  }
-  __syncthreads();
-
-  const int c_begin = blockIdx.y * a.cands_per_cta;
-  const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
-  for (int s = c_begin; s < c_end; s++) {
-    const float* cm = P.v + s * PER;
-    // T2 = Bᵀ d, column by column (d column q from smem), staged to smem
-#pragma unroll
-    for (int q = 0; q < N; q++) {
-      T dc[N];
-#pragma unroll
-      for (int j = 0; j < N; j++) dc[j] = sd[(j * N + q) * kSwThreads + tid];
-#pragma unroll
-      for (int i = 0; i < N; i++) {
-        T acc = L::zero();
-#pragma unroll
-        for (int j = 0; j < N; j++) acc = L::fma(dc[j], cm[OFF_B + i * N + j], acc);
-        st2[(i * N + q) * kSwThreads + tid] = acc;
-      }
-    }
-    T t3[M][N];
-#pragma unroll
-    for (int p = 0; p < M; p++)
-#pragma unroll
-      for (int l = 0; l < N; l++) t3[p][l] = L::zero();
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-      // U row i = (G g Gᵀ)[i,:]:  T1[i][q] = Σ_j G[i][j] g[j][q];  U[i][l] = Σ_q T1[i][q] G[l][q]
-      T t1[R];
-#pragma unroll
-      for (int q = 0; q < R; q++) {
-        T acc = L::zero();
-#pragma unroll
-        for (int j = 0; j < R; j++) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
-        t1[q] = acc;
-      }
-      T t2r[N];
-#pragma unroll
-      for (int q = 0; q < N; q++) t2r[q] = st2[(i * N + q) * kSwThreads + tid];
-#pragma unroll
-      for (int l = 0; l < N; l++) {
-        T u = L::zero();
-#pragma unroll
-        for (int q = 0; q < R; q++) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
-        // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
-        T v = L::zero();
-#pragma unroll
-        for (int q = 0; q < N; q++) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
-        const T mw = L::mul(u, v);
-        // T3[p][l] += Aᵀ[p][i] Mw[i][l]  (ascending i, from +0)
-#pragma unroll
-        for (int p = 0; p < M; p++) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
-      }
-    }
-    // Y[p][s] = Σ_l T3[p][l] Aᵀ[s][l]; score or dump
-    Stat st;
-#pragma unroll
-    for (int p = 0; p < M; p++) {
-#pragma unroll
-      for (int q = 0; q < M; q++) {
-        T y = L::zero();
-#pragma unroll
-        for (int l = 0; l < N; l++) y = L::fma(t3[p][l], cm[q * N + l], y);
-        const int o = p * M + q;
-#pragma unroll
-        for (int h = 0; h < W; h++) {
-          if (DUMP) {
-            const long long t = tile0 + tid + h * kSwThreads;
-            if (t < a.n_tiles) a.ydump[((long long)DI.idx[s] * a.n_tiles + t) * MM + o] = L::get(y, h);
-          } else {
-            st.add(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-          }
-        }
-      }
-    }
-    if (!DUMP) {
-      st.warp_reduce();
-      if ((tid & 31) == 0) {
-        double* pp = a.partial + (((long long)s * a.n_tblk + blockIdx.x) * 4 + warp) * 8;
-        write_partial(pp, st, n_valid_out);
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ K7 (1D)
-// KP pairs (of W tiles) per thread; everything in registers.
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP>
-__global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
-                                                             const __grid_constant__ IdxParam DI) {
-  using L = Lane<PAIR, NOFMA>;
-  using T = typename L::T;
-  constexpr int W = L::W;
-  constexpr int N = M + R - 1;
-  constexpr int OFF_G = M * N, OFF_B = M * N + N * R, PER = OFF_B + N * N;
-  constexpr int TPB = kSwThreads * W;
-
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const long long tile0 = (long long)blockIdx.x * TPB;
-  T d[N], g[R];
-  double y64[W][M];
-  int n_valid_out = 0;
-  {
-    float dv[W][N], gv[W][R];
-#pragma unroll
-    for (int h = 0; h < W; h++) {
-      const long long t = tile0 + tid + h * kSwThreads;
-      const bool ok = t < a.n_tiles;
-      n_valid_out += ok ? M : 0;
-#pragma unroll
-      for (int j = 0; j < N; j++) dv[h][j] = ok ? a.d[t * N + j] : 0.0f;
-#pragma unroll
-      for (int j = 0; j < R; j++) gv[h][j] = ok ? a.g[t * R + j] : 0.0f;
-#pragma unroll
-      for (int j = 0; j < M; j++) y64[h][j] = (ok && !DUMP) ? a.y64[t * M + j] : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < N; j++) {
-      if constexpr (PAIR) d[j] = L::pack(dv[0][j], dv[W - 1][j]);
-      else d[j] = dv[0][j];
-    }
-#pragma unroll
-    for (int j = 0; j < R; j++) {
-      if constexpr (PAIR) g[j] = L::pack(gv[0][j], gv[W - 1][j]);
-      else g[j] = gv[0][j];
-    }
-  }
-  n_valid_out = __reduce_add_sync(0xffffffffu, n_valid_out);
-
-  const int c_begin = blockIdx.y * a.cands_per_cta;
-  const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
-  for (int s = c_begin; s < c_end; s++) {
-    const float* cm = P.v + s * PER;
-    T mw[N];
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-      T u = L::zero(), v = L::zero();
-#pragma unroll
-      for (int j = 0; j < R; j++) u = L::fma(g[j], cm[OFF_G + i * R + j], u);
-#pragma unroll
-      for (int j = 0; j < N; j++) v = L::fma(d[j], cm[OFF_B + i * N + j], v);
-      mw[i] = L::mul(u, v);
-    }
-    Stat st;
-#pragma unroll
-    for (int p = 0; p < M; p++) {
-      T y = L::zero();
-#pragma unroll
-      for (int i = 0; i < N; i++) y = L::fma(mw[i], cm[p * N + i], y);
-#pragma unroll
-      for (int h = 0; h < W; h++) {
-        if (DUMP) {
-          const long long t = tile0 + tid + h * kSwThreads;
-          if (t < a.n_tiles) a.ydump[((long long)DI.idx[s] * a.n_tiles + t) * M + p] = L::get(y, h);
-        } else {
-          st.add(L::get(y, h), y64[h][p]);
-        }
-      }
-    }
-    if (!DUMP) {
-      st.warp_reduce();
-      if ((tid & 31) == 0) {
-        double* pp = a.partial + (((long long)s * a.n_tblk + blockIdx.x) * 4 + warp) * 8;
-        write_partial(pp, st, n_valid_out);
-      }
-    }
+  if (lane == 0) {
+    tot[0] = s;
+    tot[1] = mx;
   }
 }
 
 // ------------------------------------------------------------------ K8: finalize
-// One warp per candidate: lane l sums entries l, l+32, ... in order, then a butterfly.
-__global__ void sweep_finalize_kernel(const double* __restrict__ partial, int n_entries, int n_cand,
-                                      const __grid_constant__ IdxParam DI, double* __restrict__ d_sums,
-                                      double* __restrict__ d_maxs) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= n_cand) return;
-  const double* p = partial + (long long)warp * n_entries * 8;
-  double v[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int e = lane; e < n_entries; e += 32) {
-    const double* q = p + (long long)e * 8;
-#pragma unroll
-    for (int f = 0; f < 5; f++) v[f] += q[f];
-    v[5] = fmax(v[5], q[5]);
-    v[6] = fmax(v[6], q[6]);
+// One warp per accepted candidate: lane l sums tile groups l, l+32, ... in order, then a
+// butterfly; adds the candidate-independent reference statistics (K6b).  Acceptance
+// travels as a bitmask in the parameter space (no host->device copy).
+constexpr int kFinCands = 65536;
+struct OkMask {
+  unsigned bits[kFinCands / 32];
+};
+
+__global__ void sweep_finalize_kernel(const double* __restrict__ partial, int n_tgroups, int c0, int n_cand,
+                                      const __grid_constant__ OkMask ok, const double* __restrict__ ref_tot,
+                                      double n_outputs, double* __restrict__ d_sums, double* __restrict__ d_maxs) {
+  const int cl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (cl >= n_cand || !((ok.bits[cl >> 5] >> (cl & 31)) & 1u)) return;
+  const int c = c0 + cl;
+  const double* p = partial + (long long)c * n_tgroups * kPartial;
+  double s0 = 0.0, s1 = 0.0, m0 = 0.0, nf = 0.0;
+  for (int e = lane; e < n_tgroups; e += 32) {
+    const double* q = p + (long long)e * kPartial;
+    s0 += q[0];
+    s1 += q[1];
+    m0 = q[2] > m0 ? q[2] : m0;
+    nf += q[3];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int f = 0; f < 5; f++) v[f] += __shfl_xor_sync(0xffffffffu, v[f], o);
-    v[5] = fmax(v[5], __shfl_xor_sync(0xffffffffu, v[5], o));
-    v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], o));
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    const double mo = __shfl_xor_sync(0xffffffffu, m0, o);
+    m0 = mo > m0 ? mo : m0;
+    nf += __shfl_xor_sync(0xffffffffu, nf, o);
   }
   if (lane == 0) {
-    const int c = DI.idx[warp];
     double* su = d_sums + (long long)c * WINO_SUMS;
     double* mx = d_maxs + (long long)c * WINO_MAXS;
-    for (int f = 0; f < 5; f++) su[f] += v[f];
-    mx[0] = fmax(mx[0], v[5]);
-    mx[1] = fmax(mx[1], v[6]);
+    su[0] += s0;
+    su[1] += s1;
+    su[2] += ref_tot[0];
+    su[3] += n_outputs - nf;
+    su[4] += nf;
+    mx[0] = fmax(mx[0], m0);
+    mx[1] = fmax(mx[1], ref_tot[1]);
   }
 }
 
 // ------------------------------------------------------------------ dispatch
 namespace {
 
-typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);
-
-struct SweepCfg {
-  int dims, m, r;
-  bool pair;
-  SweepKernel k[2][2];   // [nofma][dump]
-  void (*refs)(const float*, const float*, double*, long long);
-};
-
-template <int DIMS, int M, int R, bool PAIR>
-SweepCfg make_cfg() {
-  SweepCfg c;
-  c.dims = DIMS;
-  c.m = M;
-  c.r = R;
-  c.pair = PAIR;
-  if constexpr (DIMS == 1) {
-    c.k[0][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, false, false>;
-    c.k[0][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, false, true>;
-    c.k[1][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, false>;
-    c.k[1][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, true>;
-  } else {
-    c.k[0][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, false>;
-    c.k[0][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, true>;
-    c.k[1][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, false>;
-    c.k[1][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, true>;
-  }
-  c.refs = sweep_refs_kernel<DIMS, M, R>;
-  return c;
-}
-
 const std::vector<SweepCfg>& cfgs() {
-  static const std::vector<SweepCfg> v = {
-      make_cfg<1, 1, 2, true>(), make_cfg<1, 2, 3, true>(), make_cfg<1, 3, 3, true>(),
-      make_cfg<1, 4, 3, true>(), make_cfg<1, 5, 3, true>(), make_cfg<1, 6, 3, true>(),
-      make_cfg<1, 7, 3, true>(), make_cfg<1, 8, 3, true>(), make_cfg<1, 4, 5, true>(),
-      make_cfg<1, 6, 5, true>(),
-      make_cfg<2, 1, 2, true>(), make_cfg<2, 2, 3, true>(), make_cfg<2, 3, 3, true>(),
-      make_cfg<2, 4, 3, true>(), make_cfg<2, 5, 3, true>(), make_cfg<2, 6, 3, true>(),
-      make_cfg<2, 4, 5, true>(), make_cfg<2, 6, 5, false>(), make_cfg<2, 7, 3, false>(),
-      make_cfg<2, 8, 3, false>(),
-  };
+  static const std::vector<SweepCfg> v = [] {
+    std::vector<SweepCfg> all;
+    for (auto f : {sweep_cfgs_1d, sweep_cfgs_1d_large, sweep_cfgs_2d_small, sweep_cfgs_2d_f43, sweep_cfgs_2d_large})
+      for (auto& c : f()) all.push_back(c);
+    return all;
+  }();
   return v;
 }
 
@@ -513,15 +125,53 @@ int per_cand(int m, int r) {
   return m * n + n * r + n * n;
 }
 
-size_t smem_bytes(const SweepCfg& c) {
-  if (c.dims == 1) return 0;
-  const int n = c.m + c.r - 1, W = c.pair ? 2 : 1;
-  return (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)c.m * c.m * W * kSwThreads * 8;
+int tiles_per_block(int dims, Layout lay) {
+  if (dims == 1) return kSwThreads * (lay == TSINGLE ? 1 : 2) * kKP1;
+  return kSwThreads * (lay == TPAIR ? 2 : 1);
 }
 
-long long n_tblk_of(const SweepCfg& c, int64_t n_tiles) {
-  const int tpb = kSwThreads * (c.pair ? 2 : 1);
+size_t smem_bytes(int dims, int m, int r, Layout lay) {
+  if (dims == 1) return 0;
+  const int n = m + r - 1;
+  const size_t acc = (size_t)kMaxCpc * 4 * kPartial * 8;
+  if (lay == CPAIR) return (size_t)m * m * kSwThreads * 8 + acc;
+  const int W = lay == TPAIR ? 2 : 1;
+  return (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)m * m * W * kSwThreads * 8 + acc;
+}
+
+long long n_tblk_of(int dims, Layout lay, int64_t n_tiles) {
+  const int tpb = tiles_per_block(dims, lay);
   return (n_tiles + tpb - 1) / tpb;
+}
+
+// Tile blocks per work item (a tile group).  ~200 tile groups give enough work items to
+// fill the machine; the partition depends only on (n_tiles, kernel layout), so the
+// reduction order (and every statistic) is the same for any candidate sharding.
+int tblk_per_cta(long long n_tblk) {
+  const long long target_groups = 200;
+  return (int)std::max(1LL, (n_tblk + target_groups - 1) / target_groups);
+}
+
+struct WsLayout {
+  size_t y64, partial, ref_part, ref_tot, total;
+};
+
+WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
+  const int dy = c.dims == 1 ? c.m : c.m * c.m;
+  // partial buffer sized for the layout with the most tile groups
+  long long n_tg = 1;
+  for (Layout lay : {TPAIR, TSINGLE, CPAIR}) {
+    const long long nb = std::max(n_tblk_of(c.dims, lay, n_tiles), 1LL);
+    n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
+  }
+  const long long n_ref_blocks = (n_tiles + 255) / 256;
+  WsLayout L;
+  L.y64 = 0;
+  L.partial = L.y64 + align_up((size_t)std::max<int64_t>(n_tiles, 1) * dy * sizeof(double), 256);
+  L.ref_part = L.partial + align_up((size_t)std::max(n_cand, 1) * n_tg * kPartial * sizeof(double), 256);
+  L.ref_tot = L.ref_part + align_up((size_t)std::max(n_ref_blocks, 1LL) * 2 * sizeof(double), 256);
+  L.total = L.ref_tot + 256;
+  return L;
 }
 
 }  // namespace
@@ -537,14 +187,10 @@ int sweep_max_cands_per_launch(int dims, int m, int r) {
 size_t sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles) {
   const SweepCfg* c = find_cfg(dims, m, r);
   if (!c) return 0;
-  const int dy = dims == 1 ? m : m * m;
-  const int cmax = std::min(n_cand, sweep_max_cands_per_launch(dims, m, r));
-  size_t b = align_up((size_t)(n_tiles > 0 ? n_tiles : 1) * dy * sizeof(double), 256);
-  b += align_up((size_t)(cmax > 0 ? cmax : 1) * n_tblk_of(*c, n_tiles) * 4 * 8 * sizeof(double), 256);
-  return b;
+  return ws_layout(*c, n_cand, n_tiles).total;
 }
 
-int sweep_launch(int dims, int m, int r, const float* mats, const int* cand_ok, int n_cand,
+int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_status, int n_cand,
                  const float* d_tiles, const float* g_tiles, int64_t n_tiles,
                  double* d_sums, double* d_maxs, float* d_y, void* workspace, size_t ws_bytes,
                  unsigned flags, cudaStream_t stream) {
@@ -552,58 +198,132 @@ int sweep_launch(int dims, int m, int r, const float* mats, const int* cand_ok, 
   if (!c) return set_error(WINO_E_UNSUPPORTED, "no sweep kernel for dims=%d m=%d r=%d", dims, m, r);
   const bool dump = d_y != nullptr;
   const int nofma = (flags & WINO_SWEEP_NOFMA) ? 1 : 0;
+  const Layout lay = c->variants.back().lay[nofma];
+  const int n = m + r - 1;
   const int per = per_cand(m, r);
-  const int cmax = sweep_max_cands_per_launch(dims, m, r);
+  int cmax = sweep_max_cands_per_launch(dims, m, r);
+  if (lay == CPAIR) cmax &= ~1;   // whole candidate pairs per launch
   const int dy = dims == 1 ? m : m * m;
-  const long long n_tblk = n_tiles > 0 ? n_tblk_of(*c, n_tiles) : 0;
-  if (n_tiles <= 0 || n_cand <= 0) return WINO_OK;
+  const long long n_tblk = n_tiles > 0 ? n_tblk_of(dims, lay, n_tiles) : 0;
+  const int tpc = tblk_per_cta(std::max(n_tblk, 1LL));
+  const int n_tg = (int)((n_tblk + tpc - 1) / tpc);
+  const bool work = n_tiles > 0 && n_cand > 0;
 
-  double* y64 = nullptr;
-  double* partial = nullptr;
-  if (!dump) {
-    const size_t need = sweep_workspace_bytes(dims, m, r, n_cand, n_tiles);
-    if (!workspace || ws_bytes < need)
-      return set_error(WINO_E_WORKSPACE, "sweep workspace %zu < %zu bytes", ws_bytes, need);
-    y64 = reinterpret_cast<double*>(workspace);
-    partial = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) +
-                                        align_up((size_t)n_tiles * dy * sizeof(double), 256));
+  const WsLayout L = ws_layout(*c, n_cand, n_tiles);
+  char* ws = reinterpret_cast<char*>(workspace);
+  if (!dump && work) {
+    if (!workspace || ws_bytes < L.total)
+      return set_error(WINO_E_WORKSPACE, "sweep workspace %zu < %zu bytes", ws_bytes, L.total);
   }
-  const size_t smem = smem_bytes(*c);
-  SweepKernel kern = c->k[nofma][dump ? 1 : 0];
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  double* y64 = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.y64);
+  double* partial = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.partial);
+  double* ref_part = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_part);
+  double* ref_tot = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_tot);
+  const size_t smem = smem_bytes(dims, m, r, lay);
+  if (work && smem > 48 * 1024) {
+    for (const Variant& v : c->variants) {
+      cudaError_t e = cudaFuncSetAttribute((const void*)v.k[nofma][dump ? 1 : 0],
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    }
   }
-  int launches = 0;
-  if (!dump) {
-    const int tpb = 256;
-    c->refs<<<(unsigned)((n_tiles + tpb - 1) / tpb), tpb, 0, stream>>>(d_tiles, g_tiles, y64, (long long)n_tiles);
-    launches++;
-  }
-  // candidate groups per CTA: aim for >= ~4 waves of CTAs per launch
   int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (work) {
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
 
+  int launches = 0;
+  bool refs_done = false;
   MatsParam* P = new MatsParam;
   IdxParam* DI = new IdxParam;
+  std::vector<float> chunk((size_t)cmax * per);
+  std::vector<int> ok(std::max(n_cand, 1), 0);
+  double AT[WINO_MAX_N * WINO_MAX_N], G[WINO_MAX_N * WINO_MAX_N], BT[WINO_MAX_N * WINO_MAX_N];
   int i = 0;
   int status = WINO_OK;
+  // Matrices are built chunk by chunk (a2 on the host) while the previous chunk's kernels
+  // run: launches are asynchronous, so host construction overlaps device work.
   while (i < n_cand) {
     int nc = 0;
+    uint64_t nzA = 0, nzG = 0, nzB = 0;   // union of non-zero positions over the chunk
     while (i < n_cand && nc < cmax) {
-      if (cand_ok[i]) {
-        std::copy(mats + (size_t)i * per, mats + (size_t)(i + 1) * per, P->v + nc * per);
+      const int s = build_r64(m, r, point_sets + (size_t)i * n, n, AT, G, BT);
+      cand_status[i] = s;
+      if (s == WINO_OK) {
+        ok[i] = 1;
+        float* dst = chunk.data() + (size_t)nc * per;
+        for (int t = 0; t < m * n; t++) {
+          dst[t] = (float)AT[t];
+          if (dst[t] != 0.0f) nzA |= 1ull << t;
+        }
+        for (int t = 0; t < n * r; t++) {
+          dst[m * n + t] = (float)G[t];
+          if (dst[m * n + t] != 0.0f) nzG |= 1ull << t;
+        }
+        for (int t = 0; t < n * n; t++) {
+          dst[m * n + n * r + t] = (float)BT[t];
+          if (dst[m * n + n * r + t] != 0.0f) nzB |= 1ull << t;
+        }
         DI->idx[nc] = i;
         nc++;
       }
       i++;
     }
-    if (nc == 0) break;
-    const long long want_ctas = 4LL * nsm * 2;
-    int groups = (int)std::max(1LL, std::min<long long>(nc, (want_ctas + n_tblk - 1) / n_tblk));
-    int cpc = (nc + groups - 1) / groups;
-    groups = (nc + cpc - 1) / cpc;
+    if (nc == 0 || n_tiles <= 0) continue;
+    // parameter image: per candidate, or interleaved per candidate pair
+    if (lay == CPAIR) {
+      for (int j = 0; j < (nc + 1) / 2; j++) {
+        const float* A = chunk.data() + (size_t)(2 * j) * per;
+        const float* B = (2 * j + 1 < nc) ? A + per : A;   // odd tail: duplicate (discarded)
+        float* dst = P->v + (size_t)j * per * 2;
+        for (int k = 0; k < per; k++) {
+          dst[2 * k] = A[k];
+          dst[2 * k + 1] = B[k];
+        }
+      }
+    } else {
+      std::copy(chunk.data(), chunk.data() + (size_t)nc * per, P->v);
+    }
+    if (!dump && !refs_done) {
+      const int tpb = 256;
+      const unsigned nb = (unsigned)((n_tiles + tpb - 1) / tpb);
+      const auto refs = c->refs;
+      timed_launch(dims == 1 ? "sweep_refs1d" : "sweep_refs2d", stream, [&] {
+        refs<<<nb, tpb, 0, stream>>>(d_tiles, g_tiles, y64, (long long)n_tiles, ref_part);
+        sweep_refs_total_kernel<<<1, 32, 0, stream>>>(ref_part, (int)nb, ref_tot);
+      });
+      launches += 2;
+      refs_done = true;
+    }
+    // most specialised variant whose skipped entries are zero for every candidate
+    const Variant* var = &c->variants.back();
+    for (const Variant& v : c->variants)
+      if ((v.za & nzA) == 0 && (v.zg & nzG) == 0 && (v.zb & nzB) == 0) {
+        var = &v;
+        break;
+      }
+    SweepKernel kern = var->k[nofma][dump ? 1 : 0];
+    // Work item = (up to cpc candidates, one tile group).  Persistent grid of one wave of
+    // resident CTAs walking the items round-robin; cpc is chosen (<= kMaxCpc, larger is
+    // better for amortising the tile loads) so the items fill whole rounds of the wave.
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSwThreads, smem);
+    const long long slots = (long long)std::max(occ, 1) * nsm;
+    const int step = lay == CPAIR ? 2 : 1;
+    int cpc = std::min(kMaxCpc, nc + (nc & (step - 1)));
+    double best = -1.0;
+    for (int cand = cpc; cand >= std::min(8, cpc); cand -= step) {
+      const long long items = (long long)((nc + cand - 1) / cand) * n_tg;
+      const double eff = (double)items / (double)(((items + slots - 1) / slots) * slots);
+      if (eff > best + 0.02) {
+        best = eff;
+        cpc = cand;
+      }
+      if (eff > 0.97) break;
+    }
+    const int groups = (nc + cpc - 1) / cpc;
+    const long long n_items = (long long)groups * n_tg;
     SweepArgs args;
     args.d = d_tiles;
     args.g = g_tiles;
@@ -614,21 +334,38 @@ int sweep_launch(int dims, int m, int r, const float* mats, const int* cand_ok, 
     args.n_cand = nc;
     args.cands_per_cta = cpc;
     args.n_tblk = (int)n_tblk;
-    args.ydump_cand0 = 0;
-    dim3 grid((unsigned)n_tblk, (unsigned)groups);
-    kern<<<grid, kSwThreads, smem, stream>>>(args, *P, *DI);
+    args.tblk_per_cta = tpc;
+    args.n_tgroups = n_tg;
+    args.n_cgroups = groups;
+    dim3 grid((unsigned)std::min<long long>(n_items, slots));
+    timed_launch(dims == 1 ? "sweep1d" : "sweep2d", stream,
+                 [&] { kern<<<grid, kSwThreads, smem, stream>>>(args, *P, *DI); });
     launches++;
-    if (!dump) {
-      const int threads = 256;
-      const int blocks = (nc * 32 + threads - 1) / threads;
-      sweep_finalize_kernel<<<blocks, threads, 0, stream>>>(partial, (int)(n_tblk * 4), nc, *DI, d_sums, d_maxs);
-      launches++;
-    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       status = set_error(WINO_E_CUDA, "sweep launch: %s", cudaGetErrorString(e));
       break;
     }
+  }
+  if (status == WINO_OK && !dump && refs_done) {
+    const double n_out = (double)n_tiles * dy;
+    OkMask* mask = new OkMask;
+    for (int c0 = 0; c0 < n_cand && status == WINO_OK; c0 += kFinCands) {
+      const int nc = std::min(kFinCands, n_cand - c0);
+      std::fill(mask->bits, mask->bits + kFinCands / 32, 0u);
+      for (int k = 0; k < nc; k++)
+        if (ok[c0 + k]) mask->bits[k >> 5] |= 1u << (k & 31);
+      const int threads = 256;
+      const int blocks = (int)(((long long)nc * 32 + threads - 1) / threads);
+      timed_launch("sweep_finalize", stream, [&] {
+        sweep_finalize_kernel<<<blocks, threads, 0, stream>>>(partial, n_tg, c0, nc, *mask, ref_tot, n_out, d_sums,
+                                                              d_maxs);
+      });
+      launches++;
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) status = set_error(WINO_E_CUDA, "finalize launch: %s", cudaGetErrorString(e));
+    }
+    delete mask;
   }
   delete P;
   delete DI;

@@ -1,0 +1,15 @@
+// Kernel instantiations for the sweep registry (see sweep_kernels.cuh); split across
+// translation units so nvcc compiles them in parallel.
+#include "sweep_kernels.cuh"
+
+namespace wino {
+
+std::vector<SweepCfg> sweep_cfgs_1d() {
+  return {
+      make_cfg<1, 1, 2, TPAIR>(),
+      make_cfg<1, 2, 3, TPAIR>({make_variant<1, 2, 3, TPAIR, kF23A, kF23G, kF23B>()}),
+      make_cfg<1, 4, 3, TPAIR>({make_variant<1, 4, 3, TPAIR, kF43A, kF43G, kF43B>()}),
+  };
+}
+
+}  // namespace wino

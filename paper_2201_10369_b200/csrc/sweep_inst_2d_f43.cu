@@ -1,0 +1,13 @@
+// Kernel instantiations for the sweep registry (see sweep_kernels.cuh); split across
+// translation units so nvcc compiles them in parallel.
+#include "sweep_kernels.cuh"
+
+namespace wino {
+
+std::vector<SweepCfg> sweep_cfgs_2d_f43() {
+  return {
+      make_cfg<2, 4, 3, TPAIR>({make_variant<2, 4, 3, TPAIR, kF43A, kF43G, kF43B>()}),
+  };
+}
+
+}  // namespace wino

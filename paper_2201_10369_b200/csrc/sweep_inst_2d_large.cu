@@ -1,0 +1,14 @@
+// Kernel instantiations for the sweep registry (see sweep_kernels.cuh); split across
+// translation units so nvcc compiles them in parallel.
+#include "sweep_kernels.cuh"
+
+namespace wino {
+
+std::vector<SweepCfg> sweep_cfgs_2d_large() {
+  return {
+      make_cfg<2, 3, 3, TSINGLE>(), make_cfg<2, 5, 3, TSINGLE>(), make_cfg<2, 6, 3, TSINGLE>(), make_cfg<2, 4, 5, TSINGLE>(), make_cfg<2, 6, 5, TSINGLE>(),
+      make_cfg<2, 7, 3, TSINGLE>(), make_cfg<2, 8, 3, TSINGLE>(),
+  };
+}
+
+}  // namespace wino

@@ -1,0 +1,929 @@
+// Sweep kernel templates (K7) and their registry types; included by sweep.cu and the
+// sweep_inst_*.cu translation units, which instantiate disjoint sets of kernels in
+// parallel compilation units.  See sweep.cu for the design notes.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#include "wino_internal.h"
+
+namespace wino {
+typedef unsigned long long u64;
+
+constexpr int kSwThreads = 128;        // 4 warps, one per SM sub-partition
+constexpr int kParamFloats = 7424;     // coefficient floats per launch (29696 B)
+constexpr int kMaxCandsLaunch = 512;   // + 2 KB of candidate indices: < 32764 B of params
+constexpr int kMaxCpc = 32;            // candidates per CTA (smem accumulators)
+constexpr int kPartial = 4;            // doubles per partial: s0, s1, m0, nonfin
+
+struct __align__(16) MatsParam {
+  float v[kParamFloats];
+};
+struct IdxParam {
+  int idx[kMaxCandsLaunch];
+};
+
+struct SweepArgs {
+  const float* d;
+  const float* g;
+  const double* y64;
+  float* ydump;
+  double* partial;     // [n_cand_total][n_tgroups][kPartial], indexed by global candidate
+  long long n_tiles;
+  int n_cand;          // candidates in this launch
+  int cands_per_cta;
+  int n_tblk;          // tile blocks (kSwThreads * W tiles each)
+  int tblk_per_cta;    // tile blocks per work item (a tile group)
+  int n_tgroups;
+  int n_cgroups;       // candidate groups in this launch; work items = n_cgroups * n_tgroups
+};
+
+// ------------------------------------------------------------------ lane arithmetic
+// Lane<true>: two tiles per thread (FFMA2), Lane<false>: one tile (FFMA).
+// NOFMA (paper arithmetic) uses scalar __fmul_rn/__fadd_rn: ptxas 12.9 contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2, so the pair form cannot express it.
+template <bool PAIR, bool NOFMA>
+struct Lane;
+
+template <bool NOFMA>
+struct Lane<true, NOFMA> {
+  typedef u64 T;
+  static constexpr int W = 2;
+  static __device__ __forceinline__ T pack(float a, float b) {
+    T p;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
+    return p;
+  }
+  static __device__ __forceinline__ float lo(T p) {
+    float a, b;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+    return a;
+  }
+  static __device__ __forceinline__ float hi(T p) {
+    float a, b;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+    return b;
+  }
+  static __device__ __forceinline__ T zero() { return 0ull; }
+  // acc + a * c  (c broadcast to both halves)
+  static __device__ __forceinline__ T fma(T a, float c, T acc) {
+    if (NOFMA) {
+      return pack(__fadd_rn(lo(acc), __fmul_rn(lo(a), c)), __fadd_rn(hi(acc), __fmul_rn(hi(a), c)));
+    } else {
+      T d;
+      T cc = pack(c, c);
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(cc), "l"(acc));
+      return d;
+    }
+  }
+  // elementwise a * b + (+0): the Hadamard product of the C = 1 contraction (O5)
+  static __device__ __forceinline__ T mul(T a, T b) {
+    if (NOFMA) {
+      return pack(__fadd_rn(0.0f, __fmul_rn(lo(a), lo(b))), __fadd_rn(0.0f, __fmul_rn(hi(a), hi(b))));
+    } else {
+      T d;
+      T z = 0ull;
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(z));
+      return d;
+    }
+  }
+  static __device__ __forceinline__ float get(T v, int h) { return h ? hi(v) : lo(v); }
+};
+
+template <bool NOFMA>
+struct Lane<false, NOFMA> {
+  typedef float T;
+  static constexpr int W = 1;
+  static __device__ __forceinline__ T zero() { return 0.0f; }
+  static __device__ __forceinline__ T fma(T a, float c, T acc) {
+    return NOFMA ? __fadd_rn(acc, __fmul_rn(a, c)) : __fmaf_rn(a, c, acc);
+  }
+  static __device__ __forceinline__ T mul(T a, T b) {
+    return NOFMA ? __fadd_rn(0.0f, __fmul_rn(a, b)) : __fmaf_rn(a, b, 0.0f);
+  }
+  static __device__ __forceinline__ float get(T v, int) { return v; }
+};
+
+template <uint64_t MASK>
+__device__ __forceinline__ constexpr bool nz(int k) {
+  return ((MASK >> k) & 1ull) == 0ull;
+}
+
+// ------------------------------------------------------------------ statistics
+struct Stat {
+  // two independent accumulator sets (one per tile of the pair) halve the serial fp64
+  // dependency chains; they are combined in a fixed order before the warp reduction
+  double s0[2] = {0.0, 0.0}, s1[2] = {0.0, 0.0}, m0[2] = {0.0, 0.0};
+  int nonfin = 0;
+  // fast path: no finiteness test (a non-finite e makes s0 non-finite -> careful re-run)
+  template <int K>
+  __device__ __forceinline__ void add_fast(float y32, double y64) {
+    const double e = (double)y32 - y64;
+    const double ae = fabs(e);
+    s0[K] += ae;
+    s1[K] = __fma_rn(e, e, s1[K]);
+    m0[K] = ae > m0[K] ? ae : m0[K];
+  }
+  // careful path; non-finite outputs are counted per set (set 1 in the high 16 bits)
+  template <int K>
+  __device__ __forceinline__ void add_careful(float y32, double y64) {
+    const double e = (double)y32 - y64;
+    if (isfinite(e)) {
+      const double ae = fabs(e);
+      s0[K] += ae;
+      s1[K] = __fma_rn(e, e, s1[K]);
+      m0[K] = ae > m0[K] ? ae : m0[K];
+    } else {
+      nonfin += K ? 65536 : 1;
+    }
+  }
+  __device__ __forceinline__ bool finite() const {
+    return isfinite(s0[0]) && isfinite(s1[0]) && isfinite(s0[1]) && isfinite(s1[1]);
+  }
+  // combine the two sets, then a butterfly over the warp (fixed order -> deterministic);
+  // the result is in s0[0], s1[0], m0[0]
+  __device__ __forceinline__ void warp_reduce() {
+    double a = s0[0] + s0[1], b = s1[0] + s1[1], c = m0[1] > m0[0] ? m0[1] : m0[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      const double mo = __shfl_xor_sync(0xffffffffu, c, o);
+      c = mo > c ? mo : c;
+    }
+    s0[0] = a;
+    s1[0] = b;
+    m0[0] = c;
+    nonfin = __reduce_add_sync(0xffffffffu, nonfin & 0xffff) + __reduce_add_sync(0xffffffffu, nonfin >> 16);
+  }
+};
+
+// ------------------------------------------------------------------ K6: fp64 references
+template <int DIMS, int M, int R>
+__global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict__ d, const float* __restrict__ g,
+                                                         double* __restrict__ y64, long long n_tiles,
+                                                         double* __restrict__ ref_part) {
+  constexpr int N = M + R - 1;
+  constexpr int DN = DIMS == 1 ? N : N * N, DG = DIMS == 1 ? R : R * R, DY = DIMS == 1 ? M : M * M;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0, mx = 0.0;
+  if (t < n_tiles) {
+    const float* dt = d + t * DN;
+    const float* gt = g + t * DG;
+    double* yt = y64 + t * DY;
+    if (DIMS == 1) {
+      for (int p = 0; p < M; p++) {
+        double acc = 0.0;
+        for (int j = 0; j < R; j++) acc = __dadd_rn(acc, __dmul_rn((double)gt[j], (double)dt[p + j]));
+        yt[p] = acc;
+        s += fabs(acc);
+        mx = fmax(mx, fabs(acc));
+      }
+    } else {
+      for (int p = 0; p < M; p++)
+        for (int q = 0; q < M; q++) {
+          double acc = 0.0;
+          for (int u = 0; u < R; u++)
+            for (int v = 0; v < R; v++)
+              acc = __dadd_rn(acc, __dmul_rn((double)gt[u * R + v], (double)dt[(p + u) * N + q + v]));
+          yt[p * M + q] = acc;
+          s += fabs(acc);
+          mx = fmax(mx, fabs(acc));
+        }
+    }
+  }
+  // fixed-order block reduction: warp butterflies, then thread 0 over the 8 warp results
+  __shared__ double red[2][8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s;
+    red[1][threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 8; w++) {
+      a += red[0][w];
+      b = fmax(b, red[1][w]);
+    }
+    ref_part[blockIdx.x * 2] = a;
+    ref_part[blockIdx.x * 2 + 1] = b;
+  }
+}
+
+// ------------------------------------------------------------------ K7 (2D)
+// One candidate on this thread's tile pair; scores (or dumps) the M x M outputs.
+template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T* sd,
+                                       typename Lane<PAIR, NOFMA>::T* st2, const double* sy,
+                                       const typename Lane<PAIR, NOFMA>::T (&g)[R * R], int tid, Stat& st,
+                                       float* ydump_tile0, long long tile0, long long n_tiles) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
+  constexpr int N = M + R - 1, MM = M * M;
+  constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
+  // T2 = Bᵀ d, column by column (d column q from smem), staged to smem
+#pragma unroll
+  for (int q = 0; q < N; q++) {
+    T dc[N];
+#pragma unroll
+    for (int j = 0; j < N; j++) dc[j] = sd[(j * N + q) * kSwThreads + tid];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+      T acc = L::zero();
+#pragma unroll
+      for (int j = 0; j < N; j++)
+        if (nz<ZB>(i * N + j)) acc = L::fma(dc[j], cm[OFF_B + i * N + j], acc);
+      st2[(i * N + q) * kSwThreads + tid] = acc;
+    }
+  }
+  T t3[M][N];
+#pragma unroll
+  for (int p = 0; p < M; p++)
+#pragma unroll
+    for (int l = 0; l < N; l++) t3[p][l] = L::zero();
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    // U row i = (G g Gᵀ)[i,:]:  T1[i][q] = Σ_j G[i][j] g[j][q];  U[i][l] = Σ_q T1[i][q] G[l][q]
+    T t1[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      T acc = L::zero();
+#pragma unroll
+      for (int j = 0; j < R; j++)
+        if (nz<ZG>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
+      t1[q] = acc;
+    }
+    T t2r[N];
+#pragma unroll
+    for (int q = 0; q < N; q++) t2r[q] = st2[(i * N + q) * kSwThreads + tid];
+#pragma unroll
+    for (int l = 0; l < N; l++) {
+      T u = L::zero();
+#pragma unroll
+      for (int q = 0; q < R; q++)
+        if (nz<ZG>(l * R + q)) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
+      // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
+      T v = L::zero();
+#pragma unroll
+      for (int q = 0; q < N; q++)
+        if (nz<ZB>(l * N + q)) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
+      const T mw = L::mul(u, v);
+      // T3[p][l] += Aᵀ[p][i] Mw[i][l]  (ascending i, from +0)
+#pragma unroll
+      for (int p = 0; p < M; p++)
+        if (nz<ZA>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
+    }
+  }
+  // Y[p][q] = Σ_l T3[p][l] Aᵀ[q][l]; score or dump
+#pragma unroll
+  for (int p = 0; p < M; p++) {
+#pragma unroll
+    for (int q = 0; q < M; q++) {
+      T y = L::zero();
+#pragma unroll
+      for (int l = 0; l < N; l++)
+        if (nz<ZA>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
+      const int o = p * M + q;
+#pragma unroll
+      for (int h = 0; h < W; h++) {
+        if (DUMP) {
+          const long long t = tile0 + tid + h * kSwThreads;
+          if (t < n_tiles) ydump_tile0[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
+        } else if (CAREFUL) {
+          if (h == 0) st.template add_careful<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+          else st.template add_careful<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+        } else {
+          if (h == 0) st.template add_fast<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+          else st.template add_fast<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+        }
+      }
+    }
+  }
+}
+
+// smem: sd [NN][128] T (tiles), st2 [NN][128] T (T2 staging), sy [MM][W][128] double,
+//       sacc [kMaxCpc][4 warps][kPartial] double
+template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+                                                             const __grid_constant__ IdxParam DI) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
+  constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
+  constexpr int PER = M * N + N * R + N * N;
+  constexpr int TPB = kSwThreads * W;
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sd = reinterpret_cast<T*>(smem);
+  T* st2 = sd + NN * kSwThreads;
+  double* sy = reinterpret_cast<double*>(st2 + NN * kSwThreads);
+  double* sacc = sy + MM * W * kSwThreads;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // persistent CTAs walk the (candidate group, tile group) work items round-robin
+  const int n_items = a.n_cgroups * a.n_tgroups;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+  const int c_begin = cg * a.cands_per_cta;
+  const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+  __syncthreads();  // the previous item's accumulators are flushed
+  if (!DUMP)
+    for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+
+  const int tb_begin = tg * a.tblk_per_cta;
+  const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+  for (int tb = tb_begin; tb < tb_end; tb++) {
+    const long long tile0 = (long long)tb * TPB;
+    __syncthreads();  // previous block's smem no longer in use
+    // Each thread stages its own W tiles: vector loads of the contiguous tile rows, stores
+    // [e][tid] (pairs as 8-byte words) -> conflict-free shared-memory writes.
+    {
+      bool ok[W];
+#pragma unroll
+      for (int h = 0; h < W; h++) ok[h] = tile0 + tid + h * kSwThreads < a.n_tiles;
+      if constexpr (NN % 4 == 0) {
+#pragma unroll 3
+        for (int e4 = 0; e4 < NN / 4; e4++) {
+          float4 v[W];
+#pragma unroll
+          for (int h = 0; h < W; h++)
+            v[h] = ok[h] ? __ldg(reinterpret_cast<const float4*>(a.d + (tile0 + tid + h * kSwThreads) * NN) + e4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (PAIR) {
+            sd[(e4 * 4 + 0) * kSwThreads + tid] = L::pack(v[0].x, v[W - 1].x);
+            sd[(e4 * 4 + 1) * kSwThreads + tid] = L::pack(v[0].y, v[W - 1].y);
+            sd[(e4 * 4 + 2) * kSwThreads + tid] = L::pack(v[0].z, v[W - 1].z);
+            sd[(e4 * 4 + 3) * kSwThreads + tid] = L::pack(v[0].w, v[W - 1].w);
+          } else {
+            reinterpret_cast<float*>(sd)[(e4 * 4 + 0) * kSwThreads + tid] = v[0].x;
+            reinterpret_cast<float*>(sd)[(e4 * 4 + 1) * kSwThreads + tid] = v[0].y;
+            reinterpret_cast<float*>(sd)[(e4 * 4 + 2) * kSwThreads + tid] = v[0].z;
+            reinterpret_cast<float*>(sd)[(e4 * 4 + 3) * kSwThreads + tid] = v[0].w;
+          }
+        }
+      } else {
+#pragma unroll 4
+        for (int e = 0; e < NN; e++) {
+          float v[W];
+#pragma unroll
+          for (int h = 0; h < W; h++) v[h] = ok[h] ? __ldg(a.d + (tile0 + tid + h * kSwThreads) * NN + e) : 0.0f;
+          if constexpr (PAIR) sd[e * kSwThreads + tid] = L::pack(v[0], v[W - 1]);
+          else reinterpret_cast<float*>(sd)[e * kSwThreads + tid] = v[0];
+        }
+      }
+      if (!DUMP) {
+#pragma unroll
+        for (int h = 0; h < W; h++) {
+          const double* ysrc = a.y64 + (tile0 + tid + h * kSwThreads) * MM;
+          if constexpr (MM % 2 == 0) {
+#pragma unroll 4
+            for (int o2 = 0; o2 < MM / 2; o2++) {
+              const double2 v = ok[h] ? __ldg(reinterpret_cast<const double2*>(ysrc) + o2) : make_double2(0.0, 0.0);
+              sy[((2 * o2) * W + h) * kSwThreads + tid] = v.x;
+              sy[((2 * o2 + 1) * W + h) * kSwThreads + tid] = v.y;
+            }
+          } else {
+#pragma unroll 4
+            for (int o = 0; o < MM; o++) sy[(o * W + h) * kSwThreads + tid] = ok[h] ? __ldg(ysrc + o) : 0.0;
+          }
+        }
+      }
+    }
+    T g[RR];
+#pragma unroll
+    for (int e = 0; e < RR; e++) {
+      float gv[2] = {0.0f, 0.0f};
+#pragma unroll
+      for (int h = 0; h < W; h++) {
+        const long long t = tile0 + tid + h * kSwThreads;
+        if (t < a.n_tiles) gv[h] = a.g[t * RR + e];
+      }
+      if constexpr (PAIR) g[e] = L::pack(gv[0], gv[1]);
+      else g[e] = gv[0];
+    }
+    __syncthreads();
+
+    for (int s = c_begin; s < c_end; s++) {
+      const float* cm = P.v + s * PER;
+      Stat st;
+      float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
+      eval2d<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, sd, st2, sy, g, tid, st, yd, tile0, a.n_tiles);
+      if (!DUMP) {
+        if (__any_sync(0xffffffffu, !st.finite())) {
+          st = Stat();
+          eval2d<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, sd, st2, sy, g, tid, st, nullptr, tile0, a.n_tiles);
+        }
+        st.warp_reduce();
+        if (lane == 0) {
+          double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
+          acc[0] += st.s0[0];
+          acc[1] += st.s1[0];
+          acc[2] = st.m0[0] > acc[2] ? st.m0[0] : acc[2];
+          acc[3] += (double)st.nonfin;
+        }
+      }
+    }
+  }
+  if (!DUMP) {
+    __syncthreads();
+    for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
+      double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
+      for (int w = 0; w < 4; w++) {
+        const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
+        v[0] += acc[0];
+        v[1] += acc[1];
+        v[2] = acc[2] > v[2] ? acc[2] : v[2];
+        v[3] += acc[3];
+      }
+      double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
+      for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+    }
+  }
+  }  // work items
+}
+
+// ------------------------------------------------------------------ K7 (2D, candidate pairs)
+// The production 2D kernel.  Each thread owns ONE tile (d, g in registers) and evaluates
+// TWO candidates at once: FFMA2 lanes = (candidate A, candidate B).  Coefficients arrive
+// interleaved per pair, [c_A, c_B] for every matrix entry, as one 64-bit uniform register
+// (SASS `FFMA2 R, Rd.F32, UR.F32x2, R`: the tile value is broadcast, the coefficient pair
+// is per-lane).  Nothing candidate-dependent touches shared memory: T2 is formed row by row
+// from the tile in registers, so the only shared-memory traffic is y64 (one load per
+// output per candidate pair).  Per element the dot products are the canonical O5 chains.
+namespace cp {
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 p;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
+  return p;
+}
+__device__ __forceinline__ float lo(u64 p) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+  return a;
+}
+__device__ __forceinline__ float hi(u64 p) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+  return b;
+}
+// acc + x * (cA, cB): x broadcast (tile data), coefficient pair per lane
+__device__ __forceinline__ u64 fb(float x, u64 c, u64 acc) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk(x, x)), "l"(c), "l"(acc));
+  return d;
+}
+// acc + a * c, both pairs
+__device__ __forceinline__ u64 fp(u64 a, u64 c, u64 acc) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(c), "l"(acc));
+  return d;
+}
+}  // namespace cp
+
+template <int M, int R, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__device__ __forceinline__ void eval2d_cp(const u64* __restrict__ cm, const float (&d)[(M + R - 1) * (M + R - 1)],
+                                          const float (&g)[R * R], const double* sy, int tid, Stat& st,
+                                          float* ydA, float* ydB, bool valid) {
+  constexpr int N = M + R - 1, MM = M * M;
+  constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
+  u64 t3[M][N];
+#pragma unroll
+  for (int p = 0; p < M; p++)
+#pragma unroll
+    for (int l = 0; l < N; l++) t3[p][l] = 0ull;
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    // T1[i][q] = Σ_j G[i][j] g[j][q]
+    u64 t1[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      u64 acc = 0ull;
+#pragma unroll
+      for (int j = 0; j < R; j++)
+        if (nz<ZG>(i * R + j)) acc = cp::fb(g[j * R + q], cm[OFF_G + i * R + j], acc);
+      t1[q] = acc;
+    }
+    // T2[i][q] = Σ_j Bᵀ[i][j] d[j][q]
+    u64 t2[N];
+#pragma unroll
+    for (int q = 0; q < N; q++) {
+      u64 acc = 0ull;
+#pragma unroll
+      for (int j = 0; j < N; j++)
+        if (nz<ZB>(i * N + j)) acc = cp::fb(d[j * N + q], cm[OFF_B + i * N + j], acc);
+      t2[q] = acc;
+    }
+#pragma unroll
+    for (int l = 0; l < N; l++) {
+      // U[i][l] = Σ_q T1[i][q] G[l][q];  V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
+      u64 u = 0ull, v = 0ull;
+#pragma unroll
+      for (int q = 0; q < R; q++)
+        if (nz<ZG>(l * R + q)) u = cp::fp(t1[q], cm[OFF_G + l * R + q], u);
+#pragma unroll
+      for (int q = 0; q < N; q++)
+        if (nz<ZB>(l * N + q)) v = cp::fp(t2[q], cm[OFF_B + l * N + q], v);
+      const u64 mw = cp::fp(u, v, 0ull);
+      // T3[p][l] += Aᵀ[p][i] Mw[i][l]
+#pragma unroll
+      for (int p = 0; p < M; p++)
+        if (nz<ZA>(p * N + i)) t3[p][l] = cp::fp(mw, cm[p * N + i], t3[p][l]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < M; p++) {
+#pragma unroll
+    for (int q = 0; q < M; q++) {
+      u64 y = 0ull;
+#pragma unroll
+      for (int l = 0; l < N; l++)
+        if (nz<ZA>(q * N + l)) y = cp::fp(t3[p][l], cm[q * N + l], y);
+      const int o = p * M + q;
+      if (DUMP) {
+        if (valid) {
+          ydA[o] = cp::lo(y);
+          if (ydB) ydB[o] = cp::hi(y);
+        }
+      } else {
+        const double r = sy[o * kSwThreads + tid];
+        if (CAREFUL) {
+          st.template add_careful<0>(cp::lo(y), r);
+          st.template add_careful<1>(cp::hi(y), r);
+        } else {
+          st.template add_fast<0>(cp::lo(y), r);
+          st.template add_fast<1>(cp::hi(y), r);
+        }
+      }
+    }
+  }
+}
+
+// Per-candidate (A, B) butterfly of the two accumulator sets (sets are candidates here).
+struct StatCP {
+  __device__ static __forceinline__ void reduce(Stat& st, double (&v)[2][3], int (&nf)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      v[k][0] = st.s0[k];
+      v[k][1] = st.s1[k];
+      v[k][2] = st.m0[k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        v[k][0] += __shfl_xor_sync(0xffffffffu, v[k][0], o);
+        v[k][1] += __shfl_xor_sync(0xffffffffu, v[k][1], o);
+        const double mo = __shfl_xor_sync(0xffffffffu, v[k][2], o);
+        v[k][2] = mo > v[k][2] ? mo : v[k][2];
+      }
+    }
+    // careful path counts both candidates in one counter per set: nonfin holds A in the
+    // low 16 bits and B in the high 16 bits (<= 32 x 16 outputs per warp each)
+    const int a = __reduce_add_sync(0xffffffffu, st.nonfin & 0xffff);
+    const int b = __reduce_add_sync(0xffffffffu, st.nonfin >> 16);
+    nf[0] = a;
+    nf[1] = b;
+  }
+};
+
+// smem: sy [MM][128] double, sacc [kMaxCpc][4 warps][kPartial] double
+// Coefficients: P.v as u64 pairs, pair-block j = candidates (2j, 2j+1) of the launch.
+template <int M, int R, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__global__ void __launch_bounds__(kSwThreads) sweep2d_cp_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+                                                                const __grid_constant__ IdxParam DI) {
+  constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
+  constexpr int PER = M * N + N * R + N * N;
+  constexpr int TPB = kSwThreads;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sy = reinterpret_cast<double*>(smem);
+  double* sacc = sy + MM * kSwThreads;
+  const u64* pv = reinterpret_cast<const u64*>(P.v);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = a.n_cgroups * a.n_tgroups;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+    const int c_begin = cg * a.cands_per_cta;               // even
+    const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+    __syncthreads();  // the previous item's accumulators / y64 are no longer in use
+    if (!DUMP)
+      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    const int tb_begin = tg * a.tblk_per_cta;
+    const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+    for (int tb = tb_begin; tb < tb_end; tb++) {
+      const long long t = (long long)tb * TPB + tid;
+      const bool valid = t < a.n_tiles;
+      float d[NN], g[RR];
+      if constexpr (NN % 4 == 0) {
+#pragma unroll
+        for (int e4 = 0; e4 < NN / 4; e4++) {
+          const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(a.d + t * NN) + e4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+          d[4 * e4] = v.x;
+          d[4 * e4 + 1] = v.y;
+          d[4 * e4 + 2] = v.z;
+          d[4 * e4 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NN; e++) d[e] = valid ? __ldg(a.d + t * NN + e) : 0.0f;
+      }
+#pragma unroll
+      for (int e = 0; e < RR; e++) g[e] = valid ? __ldg(a.g + t * RR + e) : 0.0f;
+      __syncthreads();  // previous tile block's y64 reads are done
+      if (!DUMP) {
+#pragma unroll
+        for (int o = 0; o < MM; o++) sy[o * kSwThreads + tid] = valid ? __ldg(a.y64 + t * MM + o) : 0.0;
+      }
+      __syncthreads();
+      for (int s = c_begin; s < c_end; s += 2) {
+        const u64* cm = pv + (s >> 1) * PER;
+        const bool has_b = s + 1 < c_end;
+        Stat st;
+        float* ydA = nullptr;
+        float* ydB = nullptr;
+        if (DUMP) {
+          ydA = a.ydump + ((long long)DI.idx[s] * a.n_tiles + t) * MM;
+          ydB = has_b ? a.ydump + ((long long)DI.idx[s + 1] * a.n_tiles + t) * MM : nullptr;
+        }
+        eval2d_cp<M, R, DUMP, false, ZA, ZG, ZB>(cm, d, g, sy, tid, st, ydA, ydB, valid);
+        if (!DUMP) {
+          if (__any_sync(0xffffffffu, !st.finite())) {
+            Stat st2;
+            eval2d_cp<M, R, false, true, ZA, ZG, ZB>(cm, d, g, sy, tid, st2, nullptr, nullptr, valid);
+            st = st2;
+          }
+          double v[2][3];
+          int nf[2];
+          StatCP::reduce(st, v, nf);
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+              if (k == 1 && !has_b) break;
+              double* acc = sacc + ((s + k - c_begin) * 4 + warp) * kPartial;
+              acc[0] += v[k][0];
+              acc[1] += v[k][1];
+              acc[2] = v[k][2] > acc[2] ? v[k][2] : acc[2];
+              acc[3] += (double)nf[k];
+            }
+          }
+        }
+      }
+    }
+    if (!DUMP) {
+      __syncthreads();
+      for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
+        double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < 4; w++) {
+          const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
+          v[0] += acc[0];
+          v[1] += acc[1];
+          v[2] = acc[2] > v[2] ? acc[2] : v[2];
+          v[3] += acc[3];
+        }
+        double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
+        for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K7 (1D)
+template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T (&d)[M + R - 1],
+                                       const typename Lane<PAIR, NOFMA>::T (&g)[R],
+                                       const double (&y64)[Lane<PAIR, NOFMA>::W][M], Stat& st, float* yd,
+                                       long long tile0, long long n_tiles, int tid) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
+  constexpr int N = M + R - 1;
+  constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
+  T mw[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    T u = L::zero(), v = L::zero();
+#pragma unroll
+    for (int j = 0; j < R; j++)
+      if (nz<ZG>(i * R + j)) u = L::fma(g[j], cm[OFF_G + i * R + j], u);
+#pragma unroll
+    for (int j = 0; j < N; j++)
+      if (nz<ZB>(i * N + j)) v = L::fma(d[j], cm[OFF_B + i * N + j], v);
+    mw[i] = L::mul(u, v);
+  }
+#pragma unroll
+  for (int p = 0; p < M; p++) {
+    T y = L::zero();
+#pragma unroll
+    for (int i = 0; i < N; i++)
+      if (nz<ZA>(p * N + i)) y = L::fma(mw[i], cm[p * N + i], y);
+#pragma unroll
+    for (int h = 0; h < W; h++) {
+      if (DUMP) {
+        const long long t = tile0 + tid + h * kSwThreads;
+        if (t < n_tiles) yd[(tid + h * kSwThreads) * M + p] = L::get(y, h);
+      } else if (CAREFUL) {
+        if (h == 0) st.template add_careful<0>(L::get(y, h), y64[h][p]);
+        else st.template add_careful<1>(L::get(y, h), y64[h][p]);
+      } else {
+        if (h == 0) st.template add_fast<0>(L::get(y, h), y64[h][p]);
+        else st.template add_fast<1>(L::get(y, h), y64[h][p]);
+      }
+    }
+  }
+}
+
+// Everything in registers; a CTA walks its tile blocks and, per block, its candidates.
+// Each thread owns kKP1 pairs of tiles, so a candidate's coefficients (uniform registers)
+// and its warp reduction are amortised over 2 * kKP1 tile evaluations.
+constexpr int kKP1 = 4;
+
+template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+                                                             const __grid_constant__ IdxParam DI) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
+  constexpr int N = M + R - 1;
+  constexpr int PER = M * N + N * R + N * N;
+  constexpr int TPB = kSwThreads * W * kKP1;
+  __shared__ double sacc[kMaxCpc * 4 * kPartial];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // persistent CTAs walk the (candidate group, tile group) work items round-robin
+  const int n_items = a.n_cgroups * a.n_tgroups;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+  const int c_begin = cg * a.cands_per_cta;
+  const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+  __syncthreads();  // the previous item's accumulators are flushed
+  if (!DUMP)
+    for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+  __syncthreads();
+
+  const int tb_begin = tg * a.tblk_per_cta;
+  const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+  for (int tb = tb_begin; tb < tb_end; tb++) {
+    T d[kKP1][N], g[kKP1][R];
+    double y64[kKP1][W][M];
+#pragma unroll
+    for (int k = 0; k < kKP1; k++) {
+      const long long tk0 = (long long)tb * TPB + k * kSwThreads * W;  // tile0 of sub-block k
+      float dv[2][N], gv[2][R];
+#pragma unroll
+      for (int h = 0; h < W; h++) {
+        const long long t = tk0 + tid + h * kSwThreads;
+        const bool ok = t < a.n_tiles;
+#pragma unroll
+        for (int j = 0; j < N; j++) dv[h][j] = ok ? __ldg(a.d + t * N + j) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < R; j++) gv[h][j] = ok ? __ldg(a.g + t * R + j) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < M; j++) y64[k][h][j] = (ok && !DUMP) ? __ldg(a.y64 + t * M + j) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        if constexpr (PAIR) d[k][j] = L::pack(dv[0][j], dv[W - 1][j]);
+        else d[k][j] = dv[0][j];
+      }
+#pragma unroll
+      for (int j = 0; j < R; j++) {
+        if constexpr (PAIR) g[k][j] = L::pack(gv[0][j], gv[W - 1][j]);
+        else g[k][j] = gv[0][j];
+      }
+    }
+    for (int s = c_begin; s < c_end; s++) {
+      const float* cm = P.v + s * PER;
+      Stat st;
+#pragma unroll
+      for (int k = 0; k < kKP1; k++) {
+        const long long tk0 = (long long)tb * TPB + k * kSwThreads * W;
+        float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tk0) * M : nullptr;
+        eval1d<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d[k], g[k], y64[k], st, yd, tk0, a.n_tiles, tid);
+      }
+      if (!DUMP) {
+        if (__any_sync(0xffffffffu, !st.finite())) {
+          st = Stat();
+#pragma unroll
+          for (int k = 0; k < kKP1; k++)
+            eval1d<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d[k], g[k], y64[k], st, nullptr, 0, a.n_tiles, tid);
+        }
+        st.warp_reduce();
+        if (lane == 0) {
+          double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
+          acc[0] += st.s0[0];
+          acc[1] += st.s1[0];
+          acc[2] = st.m0[0] > acc[2] ? st.m0[0] : acc[2];
+          acc[3] += (double)st.nonfin;
+        }
+      }
+    }
+  }
+  if (!DUMP) {
+    __syncthreads();
+    for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
+      double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
+      for (int w = 0; w < 4; w++) {
+        const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
+        v[0] += acc[0];
+        v[1] += acc[1];
+        v[2] = acc[2] > v[2] ? acc[2] : v[2];
+        v[3] += acc[3];
+      }
+      double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
+      for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+    }
+  }
+  }  // work items
+}
+
+typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);
+typedef void (*RefsKernel)(const float*, const float*, double*, long long, double*);
+
+// Kernel layouts: TPAIR = two tiles per thread (FFMA2 lanes = tiles; coefficients per
+// candidate); CPAIR = one tile per thread, two candidates per FFMA2 (coefficients
+// interleaved per candidate pair).
+enum Layout { TPAIR = 0, TSINGLE = 1, CPAIR = 2 };
+
+struct Variant {
+  uint64_t za, zg, zb;   // structural-zero masks the kernel skips (0 = dense)
+  SweepKernel k[2][2];   // [nofma][dump]
+  Layout lay[2];         // layout of k[nofma][*]
+};
+
+struct SweepCfg {
+  int dims, m, r;
+  Layout fma_layout;     // layout of the FMA (parity-mode) kernels
+  RefsKernel refs;
+  std::vector<Variant> variants;   // most specialised first, dense last
+};
+
+template <int DIMS, int M, int R, Layout LAY, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+Variant make_variant() {
+  Variant v;
+  v.za = ZA;
+  v.zg = ZG;
+  v.zb = ZB;
+  constexpr bool PAIR = LAY != TSINGLE;
+  if constexpr (DIMS == 1) {
+    v.k[0][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, false, false, ZA, ZG, ZB>;
+    v.k[0][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, false, true, ZA, ZG, ZB>;
+    v.k[1][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, false, ZA, ZG, ZB>;
+    v.k[1][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, true, ZA, ZG, ZB>;
+    v.lay[0] = v.lay[1] = PAIR ? TPAIR : TSINGLE;
+  } else if constexpr (LAY == CPAIR) {
+    v.k[0][0] = (SweepKernel)sweep2d_cp_kernel<M, R, false, ZA, ZG, ZB>;
+    v.k[0][1] = (SweepKernel)sweep2d_cp_kernel<M, R, true, ZA, ZG, ZB>;
+    // the paper-arithmetic (no-FMA) mode runs the tile-pair kernel (scalar mul/add)
+    v.k[1][0] = (SweepKernel)sweep2d_kernel<M, R, true, true, false, ZA, ZG, ZB>;
+    v.k[1][1] = (SweepKernel)sweep2d_kernel<M, R, true, true, true, ZA, ZG, ZB>;
+    v.lay[0] = CPAIR;
+    v.lay[1] = TPAIR;
+  } else {
+    v.k[0][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, false, ZA, ZG, ZB>;
+    v.k[0][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, true, ZA, ZG, ZB>;
+    v.k[1][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, false, ZA, ZG, ZB>;
+    v.k[1][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, true, ZA, ZG, ZB>;
+    v.lay[0] = v.lay[1] = PAIR ? TPAIR : TSINGLE;
+  }
+  return v;
+}
+
+template <int DIMS, int M, int R, Layout LAY>
+SweepCfg make_cfg(std::vector<Variant> specialised = {}) {
+  SweepCfg c;
+  c.dims = DIMS;
+  c.m = M;
+  c.r = R;
+  c.fma_layout = LAY;
+  c.refs = sweep_refs_kernel<DIMS, M, R>;
+  c.variants = specialised;
+  c.variants.push_back(make_variant<DIMS, M, R, LAY, 0, 0, 0>());
+  return c;
+}
+
+// Structural-zero masks of the paper's families in canonical order (bit k = row-major
+// entry k of Aᵀ / G / Bᵀ is exactly 0 for every c; generated from oracle R64 over the
+// configs[1] grid, re-checked at run time per chunk and by tests/test_abi.py):
+//   {0, ±c, ±1/c, ∞}, F(4,3):  Aᵀ 0x124920, G 0x18180, Bᵀ 0x56186a861   (570 of 834 FMAs)
+//   {0, ±c, ∞},       F(2,3):  Aᵀ 0x28,     G 0x630,   Bᵀ 0x59a9
+inline constexpr uint64_t kF43A = 0x124920ull, kF43G = 0x18180ull, kF43B = 0x56186a861ull;
+inline constexpr uint64_t kF23A = 0x28ull, kF23G = 0x630ull, kF23B = 0x59a9ull;
+
+
+// per-translation-unit registries (sweep_inst_*.cu)
+std::vector<SweepCfg> sweep_cfgs_1d();
+std::vector<SweepCfg> sweep_cfgs_1d_large();
+std::vector<SweepCfg> sweep_cfgs_2d_f43();
+std::vector<SweepCfg> sweep_cfgs_2d_small();
+std::vector<SweepCfg> sweep_cfgs_2d_large();
+
+}  // namespace wino

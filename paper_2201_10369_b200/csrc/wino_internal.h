@@ -25,9 +25,10 @@ const char* build_error_detail(int status);
 int sweep_supported(int dims, int m, int r);
 int sweep_max_cands_per_launch(int dims, int m, int r);
 size_t sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles);
-// Launches K6 (refs) once, then K7+K8 per chunk of candidates.  mats: HOST fp32
-// [n_cand][per]; cand_ok: HOST (skip where 0).
-int sweep_launch(int dims, int m, int r, const float* mats, const int* cand_ok, int n_cand,
+// Builds the candidates' matrices (R64 -> RN32) chunk by chunk on the host and launches
+// K6 (refs) once, then K7+K8 per chunk.  point_sets: HOST [n_cand][n]; cand_status: HOST
+// out (rejected candidates are skipped).
+int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_status, int n_cand,
                  const float* d_tiles, const float* g_tiles, int64_t n_tiles,
                  double* d_sums, double* d_maxs, float* d_y, void* workspace, size_t ws_bytes,
                  unsigned flags, cudaStream_t stream);
@@ -38,6 +39,24 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
                  int r, int pad, int m, const float* AT, const float* G, const float* BT,
                  void* workspace, size_t ws_bytes, double* d_sums, double* d_maxs,
                  cudaStream_t stream);
+
+// ---- kernel timing hook (capi.cpp): when enabled, brackets the launch with cudaEvents
+// on `stream` under the name `family` (read back by wino_timing_read).
+bool timing_enabled();
+void timing_record(const char* family, cudaEvent_t start, cudaEvent_t stop);
+cudaEvent_t timing_event();
+template <class F>
+void timed_launch(const char* family, cudaStream_t stream, F&& launch) {
+  if (!timing_enabled()) {
+    launch();
+    return;
+  }
+  cudaEvent_t a = timing_event(), b = timing_event();
+  cudaEventRecord(a, stream);
+  launch();
+  cudaEventRecord(b, stream);
+  timing_record(family, a, b);
+}
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

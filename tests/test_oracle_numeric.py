@@ -250,5 +250,5 @@ def test_stats_nonfinite_excluded():
     y32 = np.array([1.0, np.inf, 2.0, np.nan], dtype=np.float32)
     y64 = np.array([1.5, 1.0, 2.0, 0.0])
     s, mx = ref.stats(y32, y64)
-    assert s.tolist() == [0.5, 0.25, 3.5, 2.0, 2.0]
+    assert s.tolist() == [0.5, 0.25, 4.5, 2.0, 2.0]   # Σ|y_ref| over every output (R16)
     assert mx.tolist() == [0.5, 2.0]

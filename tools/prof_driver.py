@@ -1,0 +1,44 @@
+"""Short driver for ncu captures (tools/profile.sh): one configs[1] 2D and 1D sweep at full
+size (4096 c x 100k tiles, uniform) and one configs[2] layer, each run twice (warm-up +
+captured), through the C ABI."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2201_10369_b200 import api, points as PP  # noqa: E402
+from paper_2201_10369_b200.sweep import cfg2_specs, make_rank_sweep, run_step  # noqa: E402
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("all", "sweep"):
+        specs = cfg2_specs(synth.c_grid(4096), 100_000)
+        rs = []
+        for sp in (specs[2], specs[0]):
+            d, g = synth.random_tiles(sp.n_tiles, sp.dims, sp.n, sp.r, sp.dist, sp.seed)
+            rs.append(make_rank_sweep(sp, 0, 1, dev, d, g))
+        for _ in range(2):
+            run_step(rs)
+        torch.cuda.synchronize()
+    if what in ("all", "layer"):
+        N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
+        x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
+        xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
+        pts = PP.family_n8_cd(2.0, 1.003)
+        y = torch.empty((N, K, H, W), dtype=torch.float32, device=dev)
+        ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, W, K, r, pad, m), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
+        torch.cuda.synchronize()
+    print("prof_driver ok")
+
+
+if __name__ == "__main__":
+    main()
