@@ -371,23 +371,27 @@ def main():
                  torch.empty(rs.maxs.shape, dtype=torch.float64).pin_memory()) for rs in rsw]
     h2d = sum(p[0].numel() * 4 + p[1].numel() * 4 for p in pinned)
     d2h = sum(o[0].numel() * 8 + o[1].numel() * 8 for o in out_host)
-    e2e_ms = []
+    e2e_ms, e2e_copy_ms, host_ms = [], [], []
     barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
         flush()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a, c, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(stream)
         for rs, (pd, pg) in zip(rsw, pinned):
             rs.d_tiles.copy_(pd, non_blocking=True)
             rs.g_tiles.copy_(pg, non_blocking=True)
+        c.record(stream)
+        h0 = time.perf_counter()
         run_step(rsw)
+        host_ms.append(1e3 * (time.perf_counter() - h0))
         for rs, (hs, hm) in zip(rsw, out_host):
             hs.copy_(rs.sums, non_blocking=True)
             hm.copy_(rs.maxs, non_blocking=True)
         b.record(stream)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
+        e2e_copy_ms.append(a.elapsed_time(c))
     e2e_tot = sum(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
@@ -432,7 +436,9 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tile-evals/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_tot / args.steps,
+                    "h2d_ms_per_step": statistics.mean(e2e_copy_ms),
+                    "host_enqueue_ms_per_step": statistics.mean(host_ms)},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "step_ms": step_ms,

@@ -8,7 +8,7 @@
 //   K5 score_kernel  : y64 = fp64 direct correlation (eq:conv P:112), e = y - y64,
 //                      per-warp statistics (warp shuffles), fixed grid
 //   K8 finalize      : fixed-order reduction into d_sums/d_maxs
-// Cp = C rounded up to 8, Kp = K and Tp = T rounded up to 128; padding is zero-filled
+// Cp = C rounded up to 16, Kp = K and Tp = T rounded up to 128; padding is zero-filled
 // by K1/K2, so K3 needs no bounds checks (an fma(0, 0, acc) leaves acc unchanged up to
 // the sign of a zero).  Parity semantics: every dot product is an
 // fmaf chain from +0 in ascending index order, 2D transforms left product first.
@@ -47,14 +47,12 @@ Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m) {
   g.th = (g.Ho + m - 1) / m;
   g.tw = (g.Wo + m - 1) / m;
   g.T = (long long)N * g.th * g.tw;
-  g.Cp = (C + 7) / 8 * 8;
+  g.Cp = (C + 15) / 16 * 16;
   g.Kp = (K + 127) / 128 * 128;
   g.Tp = (g.T + 127) / 128 * 128;
   return g;
 }
 
-constexpr int kScoreBlocks = 1184;   // fixed grid (8 x 148) -> deterministic partition
-constexpr int kScoreThreads = 256;
 
 // ------------------------------------------------------------------ K1
 template <int M, int R>
@@ -152,7 +150,7 @@ __global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V,
 // Batched SGEMM  M_p[k][t] = Σ_c U_p[c][k] V_p[c][t], 128 x 128 CTA tile, BK = 8,
 // 256 threads x (8 x 8) register tile, accumulators as FFMA2 pairs along t.
 // cp.async double-buffered shared memory; every accumulator is one ascending-c fmaf chain.
-constexpr int BM = 128, BN = 128, BK = 8;
+constexpr int BM = 128, BN = 128, BK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -169,10 +167,14 @@ __device__ __forceinline__ u64 ffma2_bcast(u64 a, float c, u64 acc) {
   return d;
 }
 
+constexpr int kStages = 3;
+constexpr size_t kGemmSmem = (size_t)kStages * BK * (BM + BN) * sizeof(float);
+
 __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ U, const float* __restrict__ V,
                                                       float* __restrict__ Mo, int Cp, int Kp, long long Tp) {
-  __shared__ __align__(16) float As[2][BK][BM];
-  __shared__ __align__(16) float Bs[2][BK][BN];
+  extern __shared__ __align__(16) float gsm[];
+  float (*As)[BK][BM] = reinterpret_cast<float (*)[BK][BM]>(gsm);
+  float (*Bs)[BK][BN] = reinterpret_cast<float (*)[BK][BN]>(gsm + kStages * BK * BM);
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const long long t0 = (long long)blockIdx.x * BN;
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
   const int p = blockIdx.z;
   const float* Ap = U + (long long)p * Cp * Kp + k0;
   const float* Bp = V + (long long)p * Cp * Tp + t0;
-  // loader mapping: 256 threads x float4 = 8 rows x 128 columns
+  // loader mapping: 256 threads x 2 float4 = 16 rows x 128 columns per operand
   const int lr = tid >> 5, lc = (tid & 31) * 4;
 
   u64 acc[8][4];
@@ -190,35 +192,37 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
     for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
 
   const int nk = Cp / BK;
-  cp_async16(&As[0][lr][lc], Ap + (long long)lr * Kp + lc);
-  cp_async16(&Bs[0][lr][lc], Bp + (long long)lr * Tp + lc);
+  auto load = [&](int stage, int kt) {
+#pragma unroll
+    for (int h = 0; h < BK / 8; h++) {
+      const long long c = (long long)kt * BK + lr + 8 * h;
+      cp_async16(&As[stage][lr + 8 * h][lc], Ap + c * Kp + lc);
+      cp_async16(&Bs[stage][lr + 8 * h][lc], Bp + c * Tp + lc);
+    }
+  };
+  load(0, 0);
+  cp_async_commit();
+  if (nk > 1) load(1, 1);
   cp_async_commit();
   for (int kt = 0; kt < nk; kt++) {
-    const int cur = kt & 1;
-    if (kt + 1 < nk) {
-      const long long c1 = (long long)(kt + 1) * BK + lr;
-      cp_async16(&As[cur ^ 1][lr][lc], Ap + c1 * Kp + lc);
-      cp_async16(&Bs[cur ^ 1][lr][lc], Bp + c1 * Tp + lc);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    cp_async_wait<1>();   // stage kt has landed (only the newest group may be pending)
+    __syncthreads();      // ... for every thread; stage (kt + 2) % 3 was consumed at kt - 1
+    if (kt + 2 < nk) load((kt + 2) % kStages, kt + 2);
+    cp_async_commit();
+    const int cur = kt % kStages;
 #pragma unroll
     for (int kk = 0; kk < BK; kk++) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][64 + ty * 4]);
       const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][tx * 4]);
       const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][64 + tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const u64 b[4] = {b0.x, b0.y, b1.x, b1.y};
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const u64 bv[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
       for (int i = 0; i < 8; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j] = ffma2_bcast(b[j], a[i], acc[i][j]);
+        for (int j = 0; j < 4; j++) acc[i][j] = ffma2_bcast(bv[j], av[i], acc[i][j]);
     }
-    __syncthreads();
   }
   float* Mp = Mo + (long long)p * Kp * Tp;
 #pragma unroll
@@ -278,49 +282,78 @@ __global__ void output_kernel(const float* __restrict__ Mw, float* __restrict__ 
 }
 
 // ------------------------------------------------------------------ K5 scoring
-struct SStat {
-  double s0 = 0, s1 = 0, s2 = 0, m0 = 0, m1 = 0;
-  long long n = 0, nonfin = 0;
-};
+// fp64 direct valid correlation of the same fp32 x, w (eq:conv P:112, O7), compared with
+// the Winograd output y.  CTA = (image, 16 output channels, 16 x 16 outputs):
+// per input channel the x patch (converted to fp64) and the 16 filters are staged in
+// shared memory; each thread accumulates 16 outputs (one position, 16 channels) with DFMA
+// in the oracle's order (Σ_c Σ_u Σ_v ascending).  Statistics: warp butterflies, then a
+// fixed-order combination of the 8 warps -> one partial per CTA (deterministic).
+constexpr int kScT = 16;   // outputs per CTA side
+constexpr int kScK = 16;   // output channels per CTA
 
-__global__ void __launch_bounds__(kScoreThreads) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
-                                                              const float* __restrict__ y, Geo geo,
-                                                              double* __restrict__ partial) {
-  const long long total = (long long)geo.N * geo.K * geo.Ho * geo.Wo;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  SStat st;
-  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += stride) {
-    const int ww = (int)(o % geo.Wo);
-    const int h = (int)((o / geo.Wo) % geo.Ho);
-    const int k = (int)((o / ((long long)geo.Wo * geo.Ho)) % geo.K);
-    const int img = (int)(o / ((long long)geo.Wo * geo.Ho * geo.K));
-    double acc = 0.0;
-    for (int c = 0; c < geo.C; c++) {
-      const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
-      const float* wk = w + ((long long)k * geo.C + c) * geo.r * geo.r;
-      for (int u = 0; u < geo.r; u++) {
-        const int hh = h + u - geo.pad;
-        if (hh < 0 || hh >= geo.H) continue;
-        for (int v = 0; v < geo.r; v++) {
-          const int wx = ww + v - geo.pad;
-          if (wx < 0 || wx >= geo.W) continue;
-          acc = __fma_rn((double)__ldg(wk + u * geo.r + v), (double)__ldg(xc + (long long)hh * geo.W + wx), acc);
+template <int R>
+__global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                    const float* __restrict__ y, Geo geo,
+                                                    double* __restrict__ partial) {
+  constexpr int P = kScT + R - 1;
+  __shared__ double sx[P * P];
+  __shared__ __align__(16) double sw[R * R][kScK];
+  __shared__ double red[8][7];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tiles_w = (geo.Wo + kScT - 1) / kScT;
+  const int h0 = (blockIdx.x / tiles_w) * kScT, w0 = (blockIdx.x % tiles_w) * kScT;
+  const int k0 = blockIdx.y * kScK, img = blockIdx.z;
+  double acc[kScK];
+#pragma unroll
+  for (int k = 0; k < kScK; k++) acc[k] = 0.0;
+  for (int c = 0; c < geo.C; c++) {
+    __syncthreads();
+    const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
+    for (int idx = tid; idx < P * P; idx += 256) {
+      const int a = idx / P, b = idx - (idx / P) * P;
+      const int hh = h0 - geo.pad + a, wx = w0 - geo.pad + b;
+      sx[idx] = (hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W) ? (double)__ldg(xc + (long long)hh * geo.W + wx)
+                                                                 : 0.0;
+    }
+    for (int idx = tid; idx < kScK * R * R; idx += 256) {
+      const int kk = idx / (R * R), e = idx - kk * (R * R);
+      sw[e][kk] = (k0 + kk < geo.K) ? (double)__ldg(w + ((long long)(k0 + kk) * geo.C + c) * R * R + e) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < R; u++)
+#pragma unroll
+      for (int v = 0; v < R; v++) {
+        const double xv = sx[(ty + u) * P + tx + v];
+#pragma unroll
+        for (int k2 = 0; k2 < kScK / 2; k2++) {
+          const double2 wv = *reinterpret_cast<const double2*>(&sw[u * R + v][2 * k2]);
+          acc[2 * k2] = __fma_rn(wv.x, xv, acc[2 * k2]);
+          acc[2 * k2 + 1] = __fma_rn(wv.y, xv, acc[2 * k2 + 1]);
         }
       }
-    }
-    const double e = (double)y[o] - acc;
-    st.s2 += fabs(acc);
-    st.m1 = fmax(st.m1, fabs(acc));
-    if (isfinite(e)) {
-      st.s0 += fabs(e);
-      st.s1 = __fma_rn(e, e, st.s1);
-      st.m0 = fmax(st.m0, fabs(e));
-      st.n++;
-    } else {
-      st.nonfin++;
+  }
+  double s0 = 0, s1 = 0, s2 = 0, m0 = 0, m1 = 0, n = 0, nf = 0;
+  const int h = h0 + ty, ww = w0 + tx;
+  if (h < geo.Ho && ww < geo.Wo) {
+#pragma unroll
+    for (int k = 0; k < kScK; k++) {
+      if (k0 + k >= geo.K) break;
+      const double r = acc[k];
+      const double e = (double)y[(((long long)img * geo.K + k0 + k) * geo.Ho + h) * geo.Wo + ww] - r;
+      s2 += fabs(r);
+      m1 = fmax(m1, fabs(r));
+      if (isfinite(e)) {
+        s0 += fabs(e);
+        s1 = __fma_rn(e, e, s1);
+        m0 = fmax(m0, fabs(e));
+        n += 1.0;
+      } else {
+        nf += 1.0;
+      }
     }
   }
-  double v[7] = {st.s0, st.s1, st.s2, (double)st.n, (double)st.nonfin, st.m0, st.m1};
+  double v[7] = {s0, s1, s2, n, nf, m0, m1};
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
@@ -328,10 +361,19 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(const float* __res
     v[5] = fmax(v[5], __shfl_xor_sync(0xffffffffu, v[5], off));
     v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
   }
-  if ((threadIdx.x & 31) == 0) {
-    double* p = partial + ((long long)blockIdx.x * (kScoreThreads / 32) + (threadIdx.x >> 5)) * 8;
-#pragma unroll
-    for (int f = 0; f < 7; f++) p[f] = v[f];
+  if ((tid & 31) == 0)
+    for (int f = 0; f < 7; f++) red[tid >> 5][f] = v[f];
+  __syncthreads();
+  if (tid == 0) {
+    double t[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int wi = 0; wi < 8; wi++) {
+      for (int f = 0; f < 5; f++) t[f] += red[wi][f];
+      t[5] = fmax(t[5], red[wi][5]);
+      t[6] = fmax(t[6], red[wi][6]);
+    }
+    const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    double* p = partial + blk * 8;
+    for (int f = 0; f < 7; f++) p[f] = t[f];
     p[7] = 0.0;
   }
 }
@@ -364,17 +406,24 @@ __global__ void score_finalize_kernel(const double* __restrict__ partial, int n_
 typedef void (*FilterK)(const float*, float*, int, int, int, int, LayerMats);
 typedef void (*InputK)(const float*, float*, Geo, LayerMats);
 typedef void (*OutputK)(const float*, float*, Geo, LayerMats);
+typedef void (*ScoreK)(const float*, const float*, const float*, Geo, double*);
 
 struct LayerCfg {
   int m, r;
   FilterK fk;
   InputK ik;
   OutputK ok;
+  ScoreK sk;
 };
 
 template <int M, int R>
 LayerCfg make_layer_cfg() {
-  return LayerCfg{M, R, filter_kernel<M, R>, input_kernel<M, R>, output_kernel<M, R>};
+  return LayerCfg{M, R, filter_kernel<M, R>, input_kernel<M, R>, output_kernel<M, R>, score_kernel<R>};
+}
+
+dim3 score_grid(const Geo& g) {
+  return dim3((unsigned)(((g.Ho + kScT - 1) / kScT) * ((g.Wo + kScT - 1) / kScT)), (unsigned)((g.K + kScK - 1) / kScK),
+              (unsigned)g.N);
 }
 
 const LayerCfg kLayerCfgs[] = {
@@ -399,7 +448,8 @@ WsLayout ws_layout(const Geo& g) {
   L.v_off = L.u_off + align_up((size_t)nn * g.Cp * g.Kp * sizeof(float), 256);
   L.m_off = L.v_off + align_up((size_t)nn * g.Cp * g.Tp * sizeof(float), 256);
   L.p_off = L.m_off + align_up((size_t)nn * g.Kp * g.Tp * sizeof(float), 256);
-  L.total = L.p_off + align_up((size_t)kScoreBlocks * (kScoreThreads / 32) * 8 * sizeof(double), 256);
+  const dim3 sg = score_grid(g);
+  L.total = L.p_off + align_up((size_t)sg.x * sg.y * sg.z * 8 * sizeof(double), 256);
   return L;
 }
 
@@ -450,7 +500,13 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   }
   {
     dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
-    timed_launch("layer_gemm", stream, [&] { gemm_kernel<<<grid, 256, 0, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute((const void*)gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+      attr = true;
+    }
+    timed_launch("layer_gemm", stream,
+                 [&] { gemm_kernel<<<grid, 256, kGemmSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
     launches++;
   }
   {
@@ -460,10 +516,11 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     launches++;
   }
   if (d_sums) {
-    timed_launch("layer_score", stream,
-                 [&] { score_kernel<<<kScoreBlocks, kScoreThreads, 0, stream>>>(x, w, y, g, partial); });
+    const dim3 sg = score_grid(g);
+    const auto sk = cfg->sk;
+    timed_launch("layer_score", stream, [&] { sk<<<sg, 256, 0, stream>>>(x, w, y, g, partial); });
     timed_launch("layer_score_finalize", stream, [&] {
-      score_finalize_kernel<<<1, 32, 0, stream>>>(partial, kScoreBlocks * (kScoreThreads / 32), d_sums, d_maxs);
+      score_finalize_kernel<<<1, 32, 0, stream>>>(partial, (int)(sg.x * sg.y * sg.z), d_sums, d_maxs);
     });
     launches += 2;
   }

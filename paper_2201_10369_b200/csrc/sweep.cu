@@ -134,7 +134,6 @@ size_t smem_bytes(int dims, int m, int r, Layout lay) {
   if (dims == 1) return 0;
   const int n = m + r - 1;
   const size_t acc = (size_t)kMaxCpc * 4 * kPartial * 8;
-  if (lay == CPAIR) return (size_t)m * m * kSwThreads * 8 + acc;
   const int W = lay == TPAIR ? 2 : 1;
   return (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)m * m * W * kSwThreads * 8 + acc;
 }
@@ -160,7 +159,7 @@ WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
   const int dy = c.dims == 1 ? c.m : c.m * c.m;
   // partial buffer sized for the layout with the most tile groups
   long long n_tg = 1;
-  for (Layout lay : {TPAIR, TSINGLE, CPAIR}) {
+  for (Layout lay : {TPAIR, TSINGLE}) {
     const long long nb = std::max(n_tblk_of(c.dims, lay, n_tiles), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }
@@ -198,11 +197,11 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   if (!c) return set_error(WINO_E_UNSUPPORTED, "no sweep kernel for dims=%d m=%d r=%d", dims, m, r);
   const bool dump = d_y != nullptr;
   const int nofma = (flags & WINO_SWEEP_NOFMA) ? 1 : 0;
-  const Layout lay = c->variants.back().lay[nofma];
+  const std::vector<Variant>& variants = c->variants;
+  const Layout lay = variants.back().lay[nofma];
   const int n = m + r - 1;
   const int per = per_cand(m, r);
   int cmax = sweep_max_cands_per_launch(dims, m, r);
-  if (lay == CPAIR) cmax &= ~1;   // whole candidate pairs per launch
   const int dy = dims == 1 ? m : m * m;
   const long long n_tblk = n_tiles > 0 ? n_tblk_of(dims, lay, n_tiles) : 0;
   const int tpc = tblk_per_cta(std::max(n_tblk, 1LL));
@@ -221,7 +220,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   double* ref_tot = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_tot);
   const size_t smem = smem_bytes(dims, m, r, lay);
   if (work && smem > 48 * 1024) {
-    for (const Variant& v : c->variants) {
+    for (const Variant& v : variants) {
       cudaError_t e = cudaFuncSetAttribute((const void*)v.k[nofma][dump ? 1 : 0],
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -271,20 +270,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
       i++;
     }
     if (nc == 0 || n_tiles <= 0) continue;
-    // parameter image: per candidate, or interleaved per candidate pair
-    if (lay == CPAIR) {
-      for (int j = 0; j < (nc + 1) / 2; j++) {
-        const float* A = chunk.data() + (size_t)(2 * j) * per;
-        const float* B = (2 * j + 1 < nc) ? A + per : A;   // odd tail: duplicate (discarded)
-        float* dst = P->v + (size_t)j * per * 2;
-        for (int k = 0; k < per; k++) {
-          dst[2 * k] = A[k];
-          dst[2 * k + 1] = B[k];
-        }
-      }
-    } else {
-      std::copy(chunk.data(), chunk.data() + (size_t)nc * per, P->v);
-    }
+    std::copy(chunk.data(), chunk.data() + (size_t)nc * per, P->v);
     if (!dump && !refs_done) {
       const int tpb = 256;
       const unsigned nb = (unsigned)((n_tiles + tpb - 1) / tpb);
@@ -297,8 +283,8 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
       refs_done = true;
     }
     // most specialised variant whose skipped entries are zero for every candidate
-    const Variant* var = &c->variants.back();
-    for (const Variant& v : c->variants)
+    const Variant* var = &variants.back();
+    for (const Variant& v : variants)
       if ((v.za & nzA) == 0 && (v.zg & nzG) == 0 && (v.zb & nzB) == 0) {
         var = &v;
         break;
@@ -310,10 +296,9 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSwThreads, smem);
     const long long slots = (long long)std::max(occ, 1) * nsm;
-    const int step = lay == CPAIR ? 2 : 1;
-    int cpc = std::min(kMaxCpc, nc + (nc & (step - 1)));
+    int cpc = std::min(kMaxCpc, nc);
     double best = -1.0;
-    for (int cand = cpc; cand >= std::min(8, cpc); cand -= step) {
+    for (int cand = cpc; cand >= std::min(8, cpc); cand--) {
       const long long items = (long long)((nc + cand - 1) / cand) * n_tg;
       const double eff = (double)items / (double)(((items + slots - 1) / slots) * slots);
       if (eff > best + 0.02) {

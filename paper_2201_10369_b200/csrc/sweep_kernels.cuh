@@ -450,252 +450,6 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
   }  // work items
 }
 
-// ------------------------------------------------------------------ K7 (2D, candidate pairs)
-// The production 2D kernel.  Each thread owns ONE tile (d, g in registers) and evaluates
-// TWO candidates at once: FFMA2 lanes = (candidate A, candidate B).  Coefficients arrive
-// interleaved per pair, [c_A, c_B] for every matrix entry, as one 64-bit uniform register
-// (SASS `FFMA2 R, Rd.F32, UR.F32x2, R`: the tile value is broadcast, the coefficient pair
-// is per-lane).  Nothing candidate-dependent touches shared memory: T2 is formed row by row
-// from the tile in registers, so the only shared-memory traffic is y64 (one load per
-// output per candidate pair).  Per element the dot products are the canonical O5 chains.
-namespace cp {
-__device__ __forceinline__ u64 pk(float a, float b) {
-  u64 p;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
-  return p;
-}
-__device__ __forceinline__ float lo(u64 p) {
-  float a, b;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
-  return a;
-}
-__device__ __forceinline__ float hi(u64 p) {
-  float a, b;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
-  return b;
-}
-// acc + x * (cA, cB): x broadcast (tile data), coefficient pair per lane
-__device__ __forceinline__ u64 fb(float x, u64 c, u64 acc) {
-  u64 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk(x, x)), "l"(c), "l"(acc));
-  return d;
-}
-// acc + a * c, both pairs
-__device__ __forceinline__ u64 fp(u64 a, u64 c, u64 acc) {
-  u64 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(c), "l"(acc));
-  return d;
-}
-}  // namespace cp
-
-template <int M, int R, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
-__device__ __forceinline__ void eval2d_cp(const u64* __restrict__ cm, const float (&d)[(M + R - 1) * (M + R - 1)],
-                                          const float (&g)[R * R], const double* sy, int tid, Stat& st,
-                                          float* ydA, float* ydB, bool valid) {
-  constexpr int N = M + R - 1, MM = M * M;
-  constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
-  u64 t3[M][N];
-#pragma unroll
-  for (int p = 0; p < M; p++)
-#pragma unroll
-    for (int l = 0; l < N; l++) t3[p][l] = 0ull;
-#pragma unroll
-  for (int i = 0; i < N; i++) {
-    // T1[i][q] = Σ_j G[i][j] g[j][q]
-    u64 t1[R];
-#pragma unroll
-    for (int q = 0; q < R; q++) {
-      u64 acc = 0ull;
-#pragma unroll
-      for (int j = 0; j < R; j++)
-        if (nz<ZG>(i * R + j)) acc = cp::fb(g[j * R + q], cm[OFF_G + i * R + j], acc);
-      t1[q] = acc;
-    }
-    // T2[i][q] = Σ_j Bᵀ[i][j] d[j][q]
-    u64 t2[N];
-#pragma unroll
-    for (int q = 0; q < N; q++) {
-      u64 acc = 0ull;
-#pragma unroll
-      for (int j = 0; j < N; j++)
-        if (nz<ZB>(i * N + j)) acc = cp::fb(d[j * N + q], cm[OFF_B + i * N + j], acc);
-      t2[q] = acc;
-    }
-#pragma unroll
-    for (int l = 0; l < N; l++) {
-      // U[i][l] = Σ_q T1[i][q] G[l][q];  V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
-      u64 u = 0ull, v = 0ull;
-#pragma unroll
-      for (int q = 0; q < R; q++)
-        if (nz<ZG>(l * R + q)) u = cp::fp(t1[q], cm[OFF_G + l * R + q], u);
-#pragma unroll
-      for (int q = 0; q < N; q++)
-        if (nz<ZB>(l * N + q)) v = cp::fp(t2[q], cm[OFF_B + l * N + q], v);
-      const u64 mw = cp::fp(u, v, 0ull);
-      // T3[p][l] += Aᵀ[p][i] Mw[i][l]
-#pragma unroll
-      for (int p = 0; p < M; p++)
-        if (nz<ZA>(p * N + i)) t3[p][l] = cp::fp(mw, cm[p * N + i], t3[p][l]);
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < M; p++) {
-#pragma unroll
-    for (int q = 0; q < M; q++) {
-      u64 y = 0ull;
-#pragma unroll
-      for (int l = 0; l < N; l++)
-        if (nz<ZA>(q * N + l)) y = cp::fp(t3[p][l], cm[q * N + l], y);
-      const int o = p * M + q;
-      if (DUMP) {
-        if (valid) {
-          ydA[o] = cp::lo(y);
-          if (ydB) ydB[o] = cp::hi(y);
-        }
-      } else {
-        const double r = sy[o * kSwThreads + tid];
-        if (CAREFUL) {
-          st.template add_careful<0>(cp::lo(y), r);
-          st.template add_careful<1>(cp::hi(y), r);
-        } else {
-          st.template add_fast<0>(cp::lo(y), r);
-          st.template add_fast<1>(cp::hi(y), r);
-        }
-      }
-    }
-  }
-}
-
-// Per-candidate (A, B) butterfly of the two accumulator sets (sets are candidates here).
-struct StatCP {
-  __device__ static __forceinline__ void reduce(Stat& st, double (&v)[2][3], int (&nf)[2]) {
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-      v[k][0] = st.s0[k];
-      v[k][1] = st.s1[k];
-      v[k][2] = st.m0[k];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int k = 0; k < 2; k++) {
-        v[k][0] += __shfl_xor_sync(0xffffffffu, v[k][0], o);
-        v[k][1] += __shfl_xor_sync(0xffffffffu, v[k][1], o);
-        const double mo = __shfl_xor_sync(0xffffffffu, v[k][2], o);
-        v[k][2] = mo > v[k][2] ? mo : v[k][2];
-      }
-    }
-    // careful path counts both candidates in one counter per set: nonfin holds A in the
-    // low 16 bits and B in the high 16 bits (<= 32 x 16 outputs per warp each)
-    const int a = __reduce_add_sync(0xffffffffu, st.nonfin & 0xffff);
-    const int b = __reduce_add_sync(0xffffffffu, st.nonfin >> 16);
-    nf[0] = a;
-    nf[1] = b;
-  }
-};
-
-// smem: sy [MM][128] double, sacc [kMaxCpc][4 warps][kPartial] double
-// Coefficients: P.v as u64 pairs, pair-block j = candidates (2j, 2j+1) of the launch.
-template <int M, int R, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
-__global__ void __launch_bounds__(kSwThreads) sweep2d_cp_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
-                                                                const __grid_constant__ IdxParam DI) {
-  constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
-  constexpr int PER = M * N + N * R + N * N;
-  constexpr int TPB = kSwThreads;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* sy = reinterpret_cast<double*>(smem);
-  double* sacc = sy + MM * kSwThreads;
-  const u64* pv = reinterpret_cast<const u64*>(P.v);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_items = a.n_cgroups * a.n_tgroups;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
-    const int c_begin = cg * a.cands_per_cta;               // even
-    const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
-    __syncthreads();  // the previous item's accumulators / y64 are no longer in use
-    if (!DUMP)
-      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
-    const int tb_begin = tg * a.tblk_per_cta;
-    const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
-    for (int tb = tb_begin; tb < tb_end; tb++) {
-      const long long t = (long long)tb * TPB + tid;
-      const bool valid = t < a.n_tiles;
-      float d[NN], g[RR];
-      if constexpr (NN % 4 == 0) {
-#pragma unroll
-        for (int e4 = 0; e4 < NN / 4; e4++) {
-          const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(a.d + t * NN) + e4)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-          d[4 * e4] = v.x;
-          d[4 * e4 + 1] = v.y;
-          d[4 * e4 + 2] = v.z;
-          d[4 * e4 + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < NN; e++) d[e] = valid ? __ldg(a.d + t * NN + e) : 0.0f;
-      }
-#pragma unroll
-      for (int e = 0; e < RR; e++) g[e] = valid ? __ldg(a.g + t * RR + e) : 0.0f;
-      __syncthreads();  // previous tile block's y64 reads are done
-      if (!DUMP) {
-#pragma unroll
-        for (int o = 0; o < MM; o++) sy[o * kSwThreads + tid] = valid ? __ldg(a.y64 + t * MM + o) : 0.0;
-      }
-      __syncthreads();
-      for (int s = c_begin; s < c_end; s += 2) {
-        const u64* cm = pv + (s >> 1) * PER;
-        const bool has_b = s + 1 < c_end;
-        Stat st;
-        float* ydA = nullptr;
-        float* ydB = nullptr;
-        if (DUMP) {
-          ydA = a.ydump + ((long long)DI.idx[s] * a.n_tiles + t) * MM;
-          ydB = has_b ? a.ydump + ((long long)DI.idx[s + 1] * a.n_tiles + t) * MM : nullptr;
-        }
-        eval2d_cp<M, R, DUMP, false, ZA, ZG, ZB>(cm, d, g, sy, tid, st, ydA, ydB, valid);
-        if (!DUMP) {
-          if (__any_sync(0xffffffffu, !st.finite())) {
-            Stat st2;
-            eval2d_cp<M, R, false, true, ZA, ZG, ZB>(cm, d, g, sy, tid, st2, nullptr, nullptr, valid);
-            st = st2;
-          }
-          double v[2][3];
-          int nf[2];
-          StatCP::reduce(st, v, nf);
-          if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 2; k++) {
-              if (k == 1 && !has_b) break;
-              double* acc = sacc + ((s + k - c_begin) * 4 + warp) * kPartial;
-              acc[0] += v[k][0];
-              acc[1] += v[k][1];
-              acc[2] = v[k][2] > acc[2] ? v[k][2] : acc[2];
-              acc[3] += (double)nf[k];
-            }
-          }
-        }
-      }
-    }
-    if (!DUMP) {
-      __syncthreads();
-      for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
-        double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
-        for (int w = 0; w < 4; w++) {
-          const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
-          v[0] += acc[0];
-          v[1] += acc[1];
-          v[2] = acc[2] > v[2] ? acc[2] : v[2];
-          v[3] += acc[3];
-        }
-        double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
-        for (int f = 0; f < kPartial; f++) pp[f] = v[f];
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------ K7 (1D)
 template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
 __device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T (&d)[M + R - 1],
@@ -848,10 +602,9 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
 typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);
 typedef void (*RefsKernel)(const float*, const float*, double*, long long, double*);
 
-// Kernel layouts: TPAIR = two tiles per thread (FFMA2 lanes = tiles; coefficients per
-// candidate); CPAIR = one tile per thread, two candidates per FFMA2 (coefficients
-// interleaved per candidate pair).
-enum Layout { TPAIR = 0, TSINGLE = 1, CPAIR = 2 };
+// Kernel layouts: TPAIR = two tiles per thread (FFMA2 lanes = tiles, coefficients per
+// candidate as uniform registers); TSINGLE = one tile per thread (FFMA), for large n.
+enum Layout { TPAIR = 0, TSINGLE = 1 };
 
 struct Variant {
   uint64_t za, zg, zb;   // structural-zero masks the kernel skips (0 = dense)
@@ -879,14 +632,6 @@ Variant make_variant() {
     v.k[1][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, false, ZA, ZG, ZB>;
     v.k[1][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, true, ZA, ZG, ZB>;
     v.lay[0] = v.lay[1] = PAIR ? TPAIR : TSINGLE;
-  } else if constexpr (LAY == CPAIR) {
-    v.k[0][0] = (SweepKernel)sweep2d_cp_kernel<M, R, false, ZA, ZG, ZB>;
-    v.k[0][1] = (SweepKernel)sweep2d_cp_kernel<M, R, true, ZA, ZG, ZB>;
-    // the paper-arithmetic (no-FMA) mode runs the tile-pair kernel (scalar mul/add)
-    v.k[1][0] = (SweepKernel)sweep2d_kernel<M, R, true, true, false, ZA, ZG, ZB>;
-    v.k[1][1] = (SweepKernel)sweep2d_kernel<M, R, true, true, true, ZA, ZG, ZB>;
-    v.lay[0] = CPAIR;
-    v.lay[1] = TPAIR;
   } else {
     v.k[0][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, false, ZA, ZG, ZB>;
     v.k[0][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, true, ZA, ZG, ZB>;
