@@ -100,6 +100,12 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y,
                      const double* points, void* workspace, size_t workspace_bytes,
                      double* d_sums, double* d_maxs, void* stream);
 
+/* (2b) Network glue for BASELINE.json configs[4] (VGG-16 "ReLU + 2x2 maxpool"):
+ *   y[n][c][h][w] = max(0, max_{a,b < pool} x[n][c][pool h + a][pool w + b]), pool 1 | 2
+ *   (2 x 2 window, stride 2, floor).  x: DEVICE float[N][C][H][W], y: DEVICE
+ *   float[N][C][H/pool][W/pool].  Exact (no rounding).  Asynchronous on `stream`. */
+int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, int pool, void* stream);
+
 /* (3) Error sweep over candidate point sets on ONE device (P:465 error protocol; P:472
  * sweep; the multi-GPU driver shards candidates over ranks and all-reduces the stats).
  *   dims 1|2; point_sets: HOST double[n_cand][n] (each row obeys (1)).
@@ -132,7 +138,7 @@ int wino_last_launch_count(void);
  * bracketed by two cudaEvents recorded on its own stream and filed under its kernel
  * family: "sweep1d", "sweep2d", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
  * "layer_filter", "layer_input", "layer_gemm", "layer_output", "layer_score",
- * "layer_score_finalize".  wino_timing_read() synchronises on the recorded events and
+ * "layer_score_finalize", "relu_pool".  wino_timing_read() synchronises on the recorded events and
  * returns the summed milliseconds and launch count of one family since the last reset.
  * Returns the previous enable state / a wino_status. */
 int wino_timing_enable(int enable);

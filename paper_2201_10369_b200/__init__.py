@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     wino_error_sweep_workspace_bytes,
     wino_last_launch_count,
     wino_points_to_matrices,
+    wino_relu_pool_fp32,
     wino_supported,
     wino_sweep_outputs,
 )

@@ -79,6 +79,14 @@ def wino_conv2d_fp32(x, w, y, pad: int, m: int, points: Sequence[float], workspa
     check(st, "wino_conv2d_fp32")
 
 
+def wino_relu_pool_fp32(x, y, pool: int, stream=None) -> None:
+    """y = maxpool_pool(ReLU(x)); x [N,C,H,W], y [N,C,H/pool,W/pool] fp32 CUDA tensors."""
+    N, C, H, W = x.shape
+    if tuple(y.shape) != (N, C, H // pool, W // pool):
+        raise ValueError("output shape mismatch")
+    check(load().wino_relu_pool_fp32(_ptr(x), _ptr(y), N, C, H, W, pool, _stream_ptr(stream)), "wino_relu_pool_fp32")
+
+
 def wino_error_sweep_workspace_bytes(dims: int, m: int, r: int, n_cand: int, n_tiles: int) -> int:
     return int(load().wino_error_sweep_workspace_bytes(dims, m, r, n_cand, n_tiles))
 

@@ -169,6 +169,15 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y, int N, int C, int
                              workspace_bytes, d_sums, d_maxs, (cudaStream_t)stream));
 }
 
+int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, int pool, void* stream) {
+  reset_launches();
+  if (!x || !y) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  if (N < 1 || C < 1 || H < 1 || W < 1 || (pool != 1 && pool != 2))
+    return set_error(WINO_E_INVALID_ARG, "bad sizes or pool not 1|2");
+  if (pool == 2 && (H < 2 || W < 2)) return set_error(WINO_E_BAD_SHAPE, "pool 2 needs H, W >= 2");
+  return finish(relu_pool_launch(x, y, N, C, H, W, pool, (cudaStream_t)stream));
+}
+
 size_t wino_error_sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles) {
   if ((dims != 1 && dims != 2) || m < 1 || r < 1 || n_cand < 0 || n_tiles < 0) return 0;
   return sweep_workspace_bytes(dims, m, r, n_cand, n_tiles);

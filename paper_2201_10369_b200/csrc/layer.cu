@@ -402,6 +402,26 @@ __global__ void score_finalize_kernel(const double* __restrict__ partial, int n_
   }
 }
 
+// ------------------------------------------------------------------ K9 ReLU (+ 2x2/2 max pool)
+// Network glue of BASELINE.json configs[4] (VGG-16: "ReLU + 2x2 maxpool").  Both are exact
+// operations (max, and the sign test), so they add no rounding.  pool = 1: ReLU only.
+__global__ void relu_pool_kernel(const float* __restrict__ x, float* __restrict__ y, long long NC, int H, int W,
+                                 int pool) {
+  const int Ho = H / pool, Wo = W / pool;
+  const long long total = NC * Ho * Wo;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(o % Wo);
+    const int h = (int)((o / Wo) % Ho);
+    const long long nc = o / ((long long)Wo * Ho);
+    const float* src = x + (nc * H + (long long)h * pool) * W + (long long)w * pool;
+    float v = 0.0f;   // ReLU: max(0, ·)
+    for (int a = 0; a < pool; a++)
+      for (int b = 0; b < pool; b++) v = fmaxf(v, src[(long long)a * W + b]);
+    y[o] = v;
+  }
+}
+
 // ------------------------------------------------------------------ dispatch
 typedef void (*FilterK)(const float*, float*, int, int, int, int, LayerMats);
 typedef void (*InputK)(const float*, float*, Geo, LayerMats);
@@ -454,6 +474,20 @@ WsLayout ws_layout(const Geo& g) {
 }
 
 }  // namespace
+
+int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int pool, cudaStream_t stream) {
+  const long long total = (long long)N * C * (H / pool) * (W / pool);
+  const int threads = 256;
+  const long long blocks = std::min<long long>((total + threads - 1) / threads, 148LL * 32);
+  if (total > 0)
+    timed_launch("relu_pool", stream, [&] {
+      relu_pool_kernel<<<(unsigned)blocks, threads, 0, stream>>>(x, y, (long long)N * C, H, W, pool);
+    });
+  count_launches(total > 0 ? 1 : 0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(WINO_E_CUDA, "relu_pool launch: %s", cudaGetErrorString(e));
+  return WINO_OK;
+}
 
 int layer_supported(int m, int r) { return find_layer(m, r) != nullptr; }
 

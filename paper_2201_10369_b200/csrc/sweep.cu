@@ -252,17 +252,19 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
       if (s == WINO_OK) {
         ok[i] = 1;
         float* dst = chunk.data() + (size_t)nc * per;
+        // non-zero positions; a matrix with more than 64 entries has no specialised
+        // variant, so its mask saturates (all bits set = "nothing may be skipped")
         for (int t = 0; t < m * n; t++) {
           dst[t] = (float)AT[t];
-          if (dst[t] != 0.0f) nzA |= 1ull << t;
+          if (dst[t] != 0.0f) nzA |= t < 64 ? 1ull << t : ~0ull;
         }
         for (int t = 0; t < n * r; t++) {
           dst[m * n + t] = (float)G[t];
-          if (dst[m * n + t] != 0.0f) nzG |= 1ull << t;
+          if (dst[m * n + t] != 0.0f) nzG |= t < 64 ? 1ull << t : ~0ull;
         }
         for (int t = 0; t < n * n; t++) {
           dst[m * n + n * r + t] = (float)BT[t];
-          if (dst[m * n + n * r + t] != 0.0f) nzB |= 1ull << t;
+          if (dst[m * n + n * r + t] != 0.0f) nzB |= t < 64 ? 1ull << t : ~0ull;
         }
         DI->idx[nc] = i;
         nc++;

@@ -40,6 +40,8 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
                  void* workspace, size_t ws_bytes, double* d_sums, double* d_maxs,
                  cudaStream_t stream);
 
+int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int pool, cudaStream_t stream);
+
 // ---- kernel timing hook (capi.cpp): when enabled, brackets the launch with cudaEvents
 // on `stream` under the name `family` (read back by wino_timing_read).
 bool timing_enabled();

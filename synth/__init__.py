@@ -28,6 +28,7 @@ __all__ = [
     "integer_layer_inputs",
     "integer_tiles",
     "c_grid",
+    "vgg16_inputs",
     "VGG16_CONVS",
 ]
 
@@ -100,6 +101,15 @@ def c_grid(count: int = 4096, lo: float = 0.05, hi: float = 20.0) -> np.ndarray:
     out = [math.exp(a + i * (b - a) / (count - 1)) for i in range(count)]
     out[0], out[-1] = lo, hi
     return np.array(out, dtype=np.float64)
+
+
+def vgg16_inputs(N: int, seed: int = 0, H: int = 224):
+    """BASELINE.json configs[4]: x [N,3,H,H] ~ N(0,1) (standing in for per-channel
+    standardised images), then each layer's He-normal weights [K,C,3,3] in stack order."""
+    rng = np.random.default_rng(seed)
+    x = draw(rng, (N, 3, H, H), "normal")
+    ws = [draw(rng, (K, C, 3, 3), "normal", scale=math.sqrt(2.0 / (C * 9))) for C, K, _, _ in VGG16_CONVS]
+    return x, ws
 
 
 # VGG-16 conv stack (BASELINE.json configs[4]): (C_in, K_out, H=W, pool_after)

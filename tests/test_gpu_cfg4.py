@@ -1,0 +1,40 @@
+"""BASELINE.json configs[3] at full size: the 256 x 256 (c1, c2) grid sweeps (n = 8 and
+n = 10, 5 x 5 kernels, 100k tiles) through the C ABI; the oracle recomputes sampled
+candidates over all tiles; degenerate grid points are rejected, not fatal."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import points as OP, ref
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("template,m,maker", [("n8_c1c2_r5", 4, OP.n8_c1c2), ("n10_c1c2_r5", 6, OP.n10_c1c2)])
+def test_cfg4_grid_full_size_sampled(template, m, maker):
+    import torch
+    from paper_2201_10369_b200.sweep import SweepSpec, make_rank_sweep, run_step
+    g = synth.c_grid(256)
+    params = np.array([(a, b) for a in g for b in g])
+    sp = SweepSpec("cfg4", 2, template, params, "uniform", 100_000, seed=2)
+    d, gt = synth.random_tiles(sp.n_tiles, 2, sp.n, 5, "uniform", 2)
+    rs = make_rank_sweep(sp, 0, 1, torch.device("cuda", 0), d, gt)
+    run_step([rs])
+    torch.cuda.synchronize()
+    s = rs.sums.cpu().numpy()
+    mx = rs.maxs.cpu().numpy()
+    diag = [i * 256 + i for i in range(256)]                      # c1 == c2: duplicate points
+    assert np.all(rs.status[diag] != 0) and np.all(s[diag] == 0)
+    ok = np.flatnonzero(rs.status == 0)
+    assert len(ok) > 60000
+    rng = np.random.default_rng(7)
+    pick = sorted(rng.choice(ok, size=3, replace=False).tolist())
+    s_ref, m_ref, _ = ref.sweep(2, m, 5, [maker(*params[i]) for i in pick], d, gt)
+    for j, i in enumerate(pick):
+        assert s[i, 3] == s_ref[j, 3] and s[i, 4] == s_ref[j, 4]
+        assert np.array_equal(mx[i], m_ref[j])
+        assert abs(s[i, 0] / s_ref[j, 0] - 1) < 1e-9
+    mae = s[ok, 0] / np.where(s[ok, 3] > 0, s[ok, 3], np.nan)
+    assert np.nanmin(mae) < 1e-5 and math.isfinite(np.nanmin(mae))
