@@ -407,18 +407,21 @@ __global__ void score_finalize_kernel(const double* __restrict__ partial, int n_
 // operations (max, and the sign test), so they add no rounding.  pool = 1: ReLU only.
 __global__ void relu_pool_kernel(const float* __restrict__ x, float* __restrict__ y, long long NC, int H, int W,
                                  int pool) {
+  // grid.x covers one (n, c) plane's outputs, grid.y strides over the planes: 32-bit
+  // in-plane index math, coalesced rows
   const int Ho = H / pool, Wo = W / pool;
-  const long long total = NC * Ho * Wo;
-  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-       o += (long long)gridDim.x * blockDim.x) {
-    const int w = (int)(o % Wo);
-    const int h = (int)((o / Wo) % Ho);
-    const long long nc = o / ((long long)Wo * Ho);
-    const float* src = x + (nc * H + (long long)h * pool) * W + (long long)w * pool;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= Ho * Wo) return;
+  const int h = o / Wo, w = o - h * Wo;
+  for (long long nc = blockIdx.y; nc < NC; nc += gridDim.y) {
+    const float* src = x + nc * H * W + (h * pool) * W + w * pool;
     float v = 0.0f;   // ReLU: max(0, ·)
-    for (int a = 0; a < pool; a++)
-      for (int b = 0; b < pool; b++) v = fmaxf(v, src[(long long)a * W + b]);
-    y[o] = v;
+    if (pool == 2) {
+      v = fmaxf(fmaxf(v, fmaxf(__ldg(src), __ldg(src + 1))), fmaxf(__ldg(src + W), __ldg(src + W + 1)));
+    } else {
+      v = fmaxf(v, __ldg(src));
+    }
+    y[nc * Ho * Wo + o] = v;
   }
 }
 
@@ -478,10 +481,11 @@ WsLayout ws_layout(const Geo& g) {
 int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int pool, cudaStream_t stream) {
   const long long total = (long long)N * C * (H / pool) * (W / pool);
   const int threads = 256;
-  const long long blocks = std::min<long long>((total + threads - 1) / threads, 148LL * 32);
+  const dim3 grid((unsigned)(((H / pool) * (W / pool) + threads - 1) / threads),
+                  (unsigned)std::min<long long>((long long)N * C, 65535));
   if (total > 0)
     timed_launch("relu_pool", stream, [&] {
-      relu_pool_kernel<<<(unsigned)blocks, threads, 0, stream>>>(x, y, (long long)N * C, H, W, pool);
+      relu_pool_kernel<<<grid, threads, 0, stream>>>(x, y, (long long)N * C, H, W, pool);
     });
   count_launches(total > 0 ? 1 : 0);
   cudaError_t e = cudaGetLastError();

@@ -127,13 +127,14 @@ int per_cand(int m, int r) {
 
 int tiles_per_block(int dims, Layout lay) {
   if (dims == 1) return kSwThreads * (lay == TSINGLE ? 1 : 2) * kKP1;
-  return kSwThreads * (lay == TPAIR ? 2 : 1);
+  return kSwThreads * (lay == TSINGLE ? 1 : 2);
 }
 
 size_t smem_bytes(int dims, int m, int r, Layout lay) {
   if (dims == 1) return 0;
   const int n = m + r - 1;
   const size_t acc = (size_t)kMaxCpc * 4 * kPartial * 8;
+  if (lay == TPAIR_REG) return (size_t)m * m * 2 * kSwThreads * 8 + acc;
   const int W = lay == TPAIR ? 2 : 1;
   return (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)m * m * W * kSwThreads * 8 + acc;
 }
@@ -159,7 +160,7 @@ WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
   const int dy = c.dims == 1 ? c.m : c.m * c.m;
   // partial buffer sized for the layout with the most tile groups
   long long n_tg = 1;
-  for (Layout lay : {TPAIR, TSINGLE}) {
+  for (Layout lay : {TPAIR, TSINGLE, TPAIR_REG}) {
     const long long nb = std::max(n_tblk_of(c.dims, lay, n_tiles), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }

@@ -450,6 +450,183 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
   }  // work items
 }
 
+// ------------------------------------------------------------------ K7 (2D, tiles in registers)
+// Variant of the tile-pair kernel for small n: the thread's two tiles d stay in registers
+// and T2 is formed row by row from them (T2[i][q] = Σ_j Bᵀ[i][j] d[j][q], ascending j), so
+// no candidate-dependent data touches shared memory; only y64 is staged.  Same chains.
+template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
+                                         const typename Lane<PAIR, NOFMA>::T (&d)[(M + R - 1) * (M + R - 1)],
+                                         const typename Lane<PAIR, NOFMA>::T (&g)[R * R], const double* sy, int tid,
+                                         Stat& st, float* ydump_tile0, long long tile0, long long n_tiles) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
+  constexpr int N = M + R - 1, MM = M * M;
+  constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
+  T t3[M][N];
+#pragma unroll
+  for (int p = 0; p < M; p++)
+#pragma unroll
+    for (int l = 0; l < N; l++) t3[p][l] = L::zero();
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    T t1[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      T acc = L::zero();
+#pragma unroll
+      for (int j = 0; j < R; j++)
+        if (nz<ZG>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
+      t1[q] = acc;
+    }
+    T t2r[N];
+#pragma unroll
+    for (int q = 0; q < N; q++) {
+      T acc = L::zero();
+#pragma unroll
+      for (int j = 0; j < N; j++)
+        if (nz<ZB>(i * N + j)) acc = L::fma(d[j * N + q], cm[OFF_B + i * N + j], acc);
+      t2r[q] = acc;
+    }
+#pragma unroll
+    for (int l = 0; l < N; l++) {
+      T u = L::zero();
+#pragma unroll
+      for (int q = 0; q < R; q++)
+        if (nz<ZG>(l * R + q)) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
+      T v = L::zero();
+#pragma unroll
+      for (int q = 0; q < N; q++)
+        if (nz<ZB>(l * N + q)) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
+      const T mw = L::mul(u, v);
+#pragma unroll
+      for (int p = 0; p < M; p++)
+        if (nz<ZA>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < M; p++) {
+#pragma unroll
+    for (int q = 0; q < M; q++) {
+      T y = L::zero();
+#pragma unroll
+      for (int l = 0; l < N; l++)
+        if (nz<ZA>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
+      const int o = p * M + q;
+#pragma unroll
+      for (int h = 0; h < W; h++) {
+        if (DUMP) {
+          const long long t = tile0 + tid + h * kSwThreads;
+          if (t < n_tiles) ydump_tile0[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
+        } else if (CAREFUL) {
+          if (h == 0) st.template add_careful<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+          else st.template add_careful<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+        } else {
+          if (h == 0) st.template add_fast<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+          else st.template add_fast<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+        }
+      }
+    }
+  }
+}
+
+// smem: sy [MM][W][128] double, sacc [kMaxCpc][4 warps][kPartial] double
+template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+__global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+                                                                 const __grid_constant__ IdxParam DI) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
+  constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
+  constexpr int PER = M * N + N * R + N * N;
+  constexpr int TPB = kSwThreads * W;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sy = reinterpret_cast<double*>(smem);
+  double* sacc = sy + MM * W * kSwThreads;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = a.n_cgroups * a.n_tgroups;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+    const int c_begin = cg * a.cands_per_cta;
+    const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+    __syncthreads();  // the previous item's accumulators are flushed
+    if (!DUMP)
+      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    const int tb_begin = tg * a.tblk_per_cta;
+    const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+    for (int tb = tb_begin; tb < tb_end; tb++) {
+      const long long tile0 = (long long)tb * TPB;
+      bool ok[W];
+#pragma unroll
+      for (int h = 0; h < W; h++) ok[h] = tile0 + tid + h * kSwThreads < a.n_tiles;
+      T d[NN], g[RR];
+#pragma unroll
+      for (int e = 0; e < NN; e++) {
+        float v[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int h = 0; h < W; h++)
+          if (ok[h]) v[h] = __ldg(a.d + (tile0 + tid + h * kSwThreads) * NN + e);
+        if constexpr (PAIR) d[e] = L::pack(v[0], v[1]);
+        else d[e] = v[0];
+      }
+#pragma unroll
+      for (int e = 0; e < RR; e++) {
+        float v[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int h = 0; h < W; h++)
+          if (ok[h]) v[h] = __ldg(a.g + (tile0 + tid + h * kSwThreads) * RR + e);
+        if constexpr (PAIR) g[e] = L::pack(v[0], v[1]);
+        else g[e] = v[0];
+      }
+      // each thread stages (and later reads) only its own y64 slots: no barrier needed
+      if (!DUMP) {
+#pragma unroll
+        for (int h = 0; h < W; h++)
+#pragma unroll 4
+          for (int o = 0; o < MM; o++)
+            sy[(o * W + h) * kSwThreads + tid] = ok[h] ? __ldg(a.y64 + (tile0 + tid + h * kSwThreads) * MM + o) : 0.0;
+      }
+      for (int s = c_begin; s < c_end; s++) {
+        const float* cm = P.v + s * PER;
+        Stat st;
+        float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
+        eval2d_r<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d, g, sy, tid, st, yd, tile0, a.n_tiles);
+        if (!DUMP) {
+          if (__any_sync(0xffffffffu, !st.finite())) {
+            st = Stat();
+            eval2d_r<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d, g, sy, tid, st, nullptr, tile0, a.n_tiles);
+          }
+          st.warp_reduce();
+          if (lane == 0) {
+            double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
+            acc[0] += st.s0[0];
+            acc[1] += st.s1[0];
+            acc[2] = st.m0[0] > acc[2] ? st.m0[0] : acc[2];
+            acc[3] += (double)st.nonfin;
+          }
+        }
+      }
+    }
+    if (!DUMP) {
+      __syncthreads();
+      for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
+        double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < 4; w++) {
+          const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
+          v[0] += acc[0];
+          v[1] += acc[1];
+          v[2] = acc[2] > v[2] ? acc[2] : v[2];
+          v[3] += acc[3];
+        }
+        double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
+        for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K7 (1D)
 template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
 __device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T (&d)[M + R - 1],
@@ -603,8 +780,9 @@ typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);
 typedef void (*RefsKernel)(const float*, const float*, double*, long long, double*);
 
 // Kernel layouts: TPAIR = two tiles per thread (FFMA2 lanes = tiles, coefficients per
-// candidate as uniform registers); TSINGLE = one tile per thread (FFMA), for large n.
-enum Layout { TPAIR = 0, TSINGLE = 1 };
+// candidate as uniform registers); TSINGLE = one tile per thread (FFMA), for large n;
+// TPAIR_REG = tile pairs held in registers (sweep2d_reg_kernel), for small n.
+enum Layout { TPAIR = 0, TSINGLE = 1, TPAIR_REG = 2 };
 
 struct Variant {
   uint64_t za, zg, zb;   // structural-zero masks the kernel skips (0 = dense)
@@ -632,6 +810,12 @@ Variant make_variant() {
     v.k[1][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, false, ZA, ZG, ZB>;
     v.k[1][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, true, ZA, ZG, ZB>;
     v.lay[0] = v.lay[1] = PAIR ? TPAIR : TSINGLE;
+  } else if constexpr (LAY == TPAIR_REG) {
+    v.k[0][0] = (SweepKernel)sweep2d_reg_kernel<M, R, true, false, false, ZA, ZG, ZB>;
+    v.k[0][1] = (SweepKernel)sweep2d_reg_kernel<M, R, true, false, true, ZA, ZG, ZB>;
+    v.k[1][0] = (SweepKernel)sweep2d_reg_kernel<M, R, true, true, false, ZA, ZG, ZB>;
+    v.k[1][1] = (SweepKernel)sweep2d_reg_kernel<M, R, true, true, true, ZA, ZG, ZB>;
+    v.lay[0] = v.lay[1] = TPAIR_REG;
   } else {
     v.k[0][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, false, ZA, ZG, ZB>;
     v.k[0][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, true, ZA, ZG, ZB>;
