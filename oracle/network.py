@@ -26,9 +26,15 @@ def relu_pool(y: np.ndarray, pool: bool) -> np.ndarray:
 
 def vgg16(x, weights, points, m=6, score=True):
     """Returns (conv outputs per layer, sums [13,5], maxs [13,2])."""
-    outs, S, Mx = [], np.zeros((13, 5)), np.zeros((13, 2))
+    return stack(VGG16, x, weights, points, m, score)
+
+
+def stack(layers, x, weights, points, m=6, score=True):
+    """Generic (C, K, H, pool_after) 3x3 stack; returns (conv outputs, sums [L,5], maxs [L,2])."""
+    L = len(layers)
+    outs, S, Mx = [], np.zeros((L, 5)), np.zeros((L, 2))
     a = x
-    for li, ((C, K, _, pool), w) in enumerate(zip(VGG16, weights)):
+    for li, ((C, K, _, pool), w) in enumerate(zip(layers, weights)):
         y = ref.conv2d_wino(a, w, 1, m, points)
         if score:
             y64 = ref.conv2d_direct64(a, w, 1)

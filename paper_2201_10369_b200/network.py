@@ -19,25 +19,42 @@ VGG16 = [
 ]
 
 
+# ResNet-20-shaped plain stack for the CIFAR-sized synthetic networks of NEXT row N4
+# (ResNet-20 on CIFAR; widths 16/32/64 at 32/16/8; the stride-2 transitions are
+# replaced by 2x2 max pools because the layer is stride 1; no residual adds -- the error
+# protocol is per layer)
+RESNET20_LIKE = ([(3, 16, 32, False)] + [(16, 16, 32, False)] * 5 + [(16, 16, 32, True)]
+                 + [(16, 32, 16, False)] + [(32, 32, 16, False)] * 4 + [(32, 32, 16, True)]
+                 + [(32, 64, 8, False)] + [(64, 64, 8, False)] * 5)
+
+
 def vgg16_forward(x, weights: Sequence, points, m: int = 6, score: bool = True, keep: bool = False,
                   stream=None):
     """x: CUDA [N,3,H,H] fp32; weights: 13 CUDA [K,C,3,3] fp32.  Returns (activation after
     the last pool, sums [13,5] | None, maxs [13,2] | None, conv outputs [13] if keep)."""
+    return stack_forward(VGG16, x, weights, points, m, score, keep, stream)
+
+
+def stack_forward(layers, x, weights: Sequence, points, m: int = 6, score: bool = True, keep: bool = False,
+                  stream=None):
+    """Generic 3x3 conv stack (C, K, H, pool_after) per layer: Winograd conv (scored) ->
+    ReLU (-> 2x2 max pool).  Returns (final activation, sums [L,5], maxs [L,2], outputs)."""
     import torch
     N, _, H, W = x.shape
     dev = x.device
+    VGG = layers
     wsb = 0
     h = H
-    for (C, K, _, pool), w in zip(VGG16, weights):
+    for (C, K, _, pool), w in zip(VGG, weights):
         assert tuple(w.shape) == (K, C, 3, 3)
         wsb = max(wsb, api.wino_conv2d_workspace_bytes(N, C, h, h, K, 3, 1, m))
         h = h // 2 if pool else h
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-    sums = torch.zeros((len(VGG16), 5), dtype=torch.float64, device=dev) if score else None
-    maxs = torch.zeros((len(VGG16), 2), dtype=torch.float64, device=dev) if score else None
+    sums = torch.zeros((len(VGG), 5), dtype=torch.float64, device=dev) if score else None
+    maxs = torch.zeros((len(VGG), 2), dtype=torch.float64, device=dev) if score else None
     outs: List = []
     a = x
-    for li, ((C, K, _, pool), w) in enumerate(zip(VGG16, weights)):
+    for li, ((C, K, _, pool), w) in enumerate(zip(VGG, weights)):
         h = a.shape[2]
         y = torch.empty((N, K, h, h), dtype=torch.float32, device=dev)
         api.wino_conv2d_fp32(a, w, y, 1, m, points, ws, sums[li] if score else None,

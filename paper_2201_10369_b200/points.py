@@ -77,6 +77,22 @@ P8 = _canon([0.0, -1.0, 1.0, 0.5, -0.5, 2.0, -2.0])
 P10 = _canon([0.0, -1.0, 1.0, 0.5, -0.5, 2.0, -2.0, -0.25, 4.0])
 
 
+def chebyshev(n: int) -> List[float]:
+    """n - 1 Chebyshev nodes x_k = cos((2k - 1) pi / (2(n - 1))), k = 1..n-1, plus
+    the formal ∞ (modified algorithm).  Computed for k <= ceil((n-1)/2) and mirrored by
+    negation, so the set is exactly symmetric and the middle node of an odd count is
+    exactly 0 (reading X24)."""
+    q = n - 1
+    if q < 1:
+        raise TemplateError("n >= 2")
+    half = []
+    for k in range(1, (q + 1) // 2 + 1):
+        half.append(math.cos((2 * k - 1) * math.pi / (2 * q)))
+    nodes = [v for v in half if not (q % 2 == 1 and v == half[-1])] if q % 2 == 1 else half
+    fin = nodes + [-v for v in nodes] + ([0.0] if q % 2 == 1 else [])
+    return _canon(fin)
+
+
 def instantiate(maker: Callable[..., List[float]], params) -> tuple:
     """Instantiate a template over parameter tuples.  Returns (point_sets [S][n] as a list,
     ok flags): a degenerate parameter gives a row of NaNs (rejected by the ABI as

@@ -112,6 +112,16 @@ def vgg16_inputs(N: int, seed: int = 0, H: int = 224):
     return x, ws
 
 
+def stack_inputs(layers, N: int, seed: int = 0):
+    """Synthetic conv stack inputs: x [N, C0, H0, H0] ~ N(0,1), He-normal weights per layer
+    (NEXT row N4: CIFAR-shaped stand-ins, no dataset items, no trained weights)."""
+    rng = np.random.default_rng(seed)
+    C0, _, H0, _ = layers[0]
+    x = draw(rng, (N, C0, H0, H0), "normal")
+    ws = [draw(rng, (K, C, 3, 3), "normal", scale=math.sqrt(2.0 / (C * 9))) for C, K, _, _ in layers]
+    return x, ws
+
+
 # VGG-16 conv stack (BASELINE.json configs[4]): (C_in, K_out, H=W, pool_after)
 VGG16_CONVS = [
     (3, 64, 224, False), (64, 64, 224, True),

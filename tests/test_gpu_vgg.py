@@ -44,3 +44,23 @@ def test_relu_pool_exact():
         api.wino_relu_pool_fp32(xd, y, pool)
         torch.cuda.synchronize()
         assert np.array_equal(y.cpu().numpy(), ON.relu_pool(x, pool == 2))
+
+
+def test_resnet20_like_stack_chebyshev_and_n5():
+    """NEXT row N4 stack (CIFAR-shaped synthetic inputs): bit-identical to the oracle chain
+    for the Chebyshev nodes and the n = 5 proposed set, first 8 layers, 3 images."""
+    import torch
+    from paper_2201_10369_b200 import network, points as PP
+    layers = network.RESNET20_LIKE[:8]
+    x, ws = synth.stack_inputs(layers, 3, seed=1)
+    dev = torch.device("cuda", 0)
+    for m, pts in ((2, PP.chebyshev(4)), (3, sorted([0.0, 1.0, -1.0, -2.0]) + [float("inf")]),
+                   (6, PP.chebyshev(8))):
+        _, s, mx, ys = network.stack_forward(layers, torch.from_numpy(x).to(dev),
+                                             [torch.from_numpy(w).to(dev) for w in ws], pts, m=m, keep=True)
+        torch.cuda.synchronize()
+        ys_ref, s_ref, m_ref = ON.stack(layers, x, ws, pts, m=m)
+        s = s.cpu().numpy()
+        for li in range(len(layers)):
+            assert np.array_equal(ys[li].cpu().numpy(), ys_ref[li]), (m, li)
+            assert abs(s[li, 0] / s_ref[li, 0] - 1) < 1e-9

@@ -252,3 +252,19 @@ def test_stats_nonfinite_excluded():
     s, mx = ref.stats(y32, y64)
     assert s.tolist() == [0.5, 0.25, 4.5, 2.0, 2.0]   # Σ|y_ref| over every output (R16)
     assert mx.tolist() == [0.5, 2.0]
+
+
+def test_chebyshev_nodes():
+    """x_k = cos((2k-1) pi / 2n); our sets use n-1 nodes + inf (reading X24): exactly
+    symmetric, the middle node exactly 0, and each node a root of the Chebyshev polynomial."""
+    from paper_2201_10369_b200 import points as PP
+    for n in range(3, 11):
+        p = PP.chebyshev(n)
+        assert p[-1] == INF and len(p) == n
+        fin = p[:-1]
+        assert fin == sorted(-v for v in fin)
+        q = n - 1
+        for v in fin:
+            assert abs(math.cos(q * math.acos(v))) < 1e-12
+        if q % 2 == 1:
+            assert 0.0 in fin
