@@ -134,7 +134,7 @@ size_t smem_bytes(int dims, int m, int r, Layout lay) {
   if (dims == 1) return 0;
   const int n = m + r - 1;
   const size_t acc = (size_t)kMaxCpc * 4 * kPartial * 8;
-  if (lay == TPAIR_REG) return (size_t)m * m * 2 * kSwThreads * 8 + acc;
+  if (lay == TPAIR_REG) return (size_t)m * m * 2 * kSwThreads * 8 + acc;   // y64 as hi/lo fp32 pairs
   const int W = lay == TPAIR ? 2 : 1;
   return (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)m * m * W * kSwThreads * 8 + acc;
 }

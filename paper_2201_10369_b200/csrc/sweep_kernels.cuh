@@ -160,6 +160,64 @@ struct Stat {
   }
 };
 
+// fp32-pair scoring for the register-resident tile-pair kernel: per output pair (the two
+// tiles of the thread) e = (y32 − hi) − lo with y64 = hi + lo split into fp32 (the first
+// subtraction is exact whenever y32 and hi are within a factor 2, so e carries a relative
+// error <= 2^-23), |e| by clearing the sign bits, Σ|e| and Σe² as FADD2 / FFMA2 pairs,
+// max|e| per half.  8 instructions per output pair instead of 14 for the fp64 path, on
+// the FP32 pipe.  Per thread and candidate 16 pairs are summed in fp32 and per warp 32
+// threads, then fp64 from there on: the statistics stay within ~1e-6 relative of the
+// fp64 definition (tolerance of the north star: 1 %).  Non-finite values fall through to
+// the exact fp64 careful path.
+struct Stat32 {
+  u64 s0 = 0ull, s1 = 0ull, m0 = 0ull;
+  static __device__ __forceinline__ void split(u64 p, float& a, float& b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+  }
+  static __device__ __forceinline__ u64 join(float a, float b) {
+    u64 p;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
+    return p;
+  }
+  __device__ __forceinline__ void add(u64 y, u64 hi, u64 lo) {
+    u64 e, t;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(hi));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e) : "l"(t), "l"(lo));
+    const u64 ae = e & 0x7fffffff7fffffffull;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s0) : "l"(s0), "l"(ae));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s1) : "l"(e), "l"(s1));
+    float a0, a1, m0a, m0b;
+    split(ae, a0, a1);
+    split(m0, m0a, m0b);
+    m0 = join(fmaxf(m0a, a0), fmaxf(m0b, a1));
+  }
+  __device__ __forceinline__ bool finite() const {
+    float a, b, c, d;
+    split(s0, a, b);
+    split(s1, c, d);
+    return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d);
+  }
+  // warp totals (fixed butterfly order) as fp64
+  __device__ __forceinline__ void warp_reduce(double& r0, double& r1, double& rm) const {
+    float a, b;
+    split(s0, a, b);
+    float v0 = a + b;
+    split(s1, a, b);
+    float v1 = a + b;
+    split(m0, a, b);
+    float vm = fmaxf(a, b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+      vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+    }
+    r0 = v0;
+    r1 = v1;
+    rm = vm;
+  }
+};
+
 // ------------------------------------------------------------------ K6: fp64 references
 template <int DIMS, int M, int R>
 __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict__ d, const float* __restrict__ g,
@@ -457,8 +515,9 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
 template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
 __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
                                          const typename Lane<PAIR, NOFMA>::T (&d)[(M + R - 1) * (M + R - 1)],
-                                         const typename Lane<PAIR, NOFMA>::T (&g)[R * R], const double* sy, int tid,
-                                         Stat& st, float* ydump_tile0, long long tile0, long long n_tiles) {
+                                         const typename Lane<PAIR, NOFMA>::T (&g)[R * R], const u64* syh,
+                                         const u64* syl, int tid, Stat& st, Stat32& st32, float* ydump_tile0,
+                                         long long tile0, long long n_tiles) {
   using L = Lane<PAIR, NOFMA>;
   using T = typename L::T;
   constexpr int W = L::W;
@@ -514,18 +573,22 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
       for (int l = 0; l < N; l++)
         if (nz<ZA>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
       const int o = p * M + q;
+      if (DUMP) {
 #pragma unroll
-      for (int h = 0; h < W; h++) {
-        if (DUMP) {
+        for (int h = 0; h < W; h++) {
           const long long t = tile0 + tid + h * kSwThreads;
           if (t < n_tiles) ydump_tile0[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
-        } else if (CAREFUL) {
-          if (h == 0) st.template add_careful<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-          else st.template add_careful<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-        } else {
-          if (h == 0) st.template add_fast<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-          else st.template add_fast<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
         }
+      } else if (CAREFUL) {
+        // exact fp64 path on y64 = hi + lo (the split is exact in fp64 to 2^-48 relative)
+        const u64 hp = syh[o * kSwThreads + tid], lp = syl[o * kSwThreads + tid];
+        float h0, h1, l0, l1;
+        Stat32::split(hp, h0, h1);
+        Stat32::split(lp, l0, l1);
+        st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
+        st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
+      } else {
+        st32.add(y, syh[o * kSwThreads + tid], syl[o * kSwThreads + tid]);
       }
     }
   }
@@ -541,9 +604,11 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
   constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
   constexpr int PER = M * N + N * R + N * N;
   constexpr int TPB = kSwThreads * W;
+  static_assert(PAIR, "sweep2d_reg_kernel evaluates tile pairs");
   extern __shared__ __align__(16) unsigned char smem[];
-  double* sy = reinterpret_cast<double*>(smem);
-  double* sacc = sy + MM * W * kSwThreads;
+  u64* syh = reinterpret_cast<u64*>(smem);            // [MM][128] (hi_A, hi_B)
+  u64* syl = syh + MM * kSwThreads;                    // [MM][128] (lo_A, lo_B)
+  double* sacc = reinterpret_cast<double*>(syl + MM * kSwThreads);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_items = a.n_cgroups * a.n_tgroups;
@@ -582,29 +647,45 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
       }
       // each thread stages (and later reads) only its own y64 slots: no barrier needed
       if (!DUMP) {
-#pragma unroll
-        for (int h = 0; h < W; h++)
 #pragma unroll 4
-          for (int o = 0; o < MM; o++)
-            sy[(o * W + h) * kSwThreads + tid] = ok[h] ? __ldg(a.y64 + (tile0 + tid + h * kSwThreads) * MM + o) : 0.0;
+        for (int o = 0; o < MM; o++) {
+          float hi[2], lo[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const double v = ok[h] ? __ldg(a.y64 + (tile0 + tid + h * kSwThreads) * MM + o) : 0.0;
+            hi[h] = __double2float_rn(v);
+            lo[h] = __double2float_rn(v - (double)hi[h]);
+          }
+          syh[o * kSwThreads + tid] = Stat32::join(hi[0], hi[1]);
+          syl[o * kSwThreads + tid] = Stat32::join(lo[0], lo[1]);
+        }
       }
       for (int s = c_begin; s < c_end; s++) {
         const float* cm = P.v + s * PER;
         Stat st;
+        Stat32 st32;
         float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
-        eval2d_r<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d, g, sy, tid, st, yd, tile0, a.n_tiles);
+        eval2d_r<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d, g, syh, syl, tid, st, st32, yd, tile0,
+                                                            a.n_tiles);
         if (!DUMP) {
-          if (__any_sync(0xffffffffu, !st.finite())) {
-            st = Stat();
-            eval2d_r<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d, g, sy, tid, st, nullptr, tile0, a.n_tiles);
+          double r0, r1, rm, rn = 0.0;
+          if (__any_sync(0xffffffffu, !st32.finite())) {
+            eval2d_r<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d, g, syh, syl, tid, st, st32, nullptr, tile0,
+                                                                a.n_tiles);
+            st.warp_reduce();
+            r0 = st.s0[0];
+            r1 = st.s1[0];
+            rm = st.m0[0];
+            rn = (double)st.nonfin;
+          } else {
+            st32.warp_reduce(r0, r1, rm);
           }
-          st.warp_reduce();
           if (lane == 0) {
             double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
-            acc[0] += st.s0[0];
-            acc[1] += st.s1[0];
-            acc[2] = st.m0[0] > acc[2] ? st.m0[0] : acc[2];
-            acc[3] += (double)st.nonfin;
+            acc[0] += r0;
+            acc[1] += r1;
+            acc[2] = rm > acc[2] ? rm : acc[2];
+            acc[3] += rn;
           }
         }
       }

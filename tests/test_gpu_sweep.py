@@ -1,6 +1,6 @@
 """GPU parity of the error sweep (wino_error_sweep / wino_sweep_outputs) against the
 oracle: per-element fp32 outputs bit-identical (O5 semantics), statistics within the
-north-star tolerance (MAE within 1% relative; we assert 1e-9), edge cases.  Calls go
+north-star tolerance (MAE within 1% relative; we assert 1e-5), edge cases.  Calls go
 through the C ABI (paper_2201_10369_b200.api)."""
 import math
 
@@ -54,14 +54,21 @@ def _grid_subset(k=48):
     return [float(g[i]) for i in idx]
 
 
+# Statistics tolerances (north star: MAE within 1 % relative).  Most sweep kernels score in
+# fp64 (agreement ~1e-15); the F(4x4,3x3) production kernel scores tile pairs in fp32 within
+# a warp-candidate (e to 2^-23 relative, sums to ~1e-6), hence 1e-5 / 1e-6.
+RTOL_SUM, RTOL_MAX = 1e-5, 1e-6
+
+
 def _assert_stats_close(s_gpu, m_gpu, s_ref, m_ref):
     assert np.array_equal(s_gpu[:, 3], s_ref[:, 3])       # n_scored exact
     assert np.array_equal(s_gpu[:, 4], s_ref[:, 4])       # n_nonfinite exact
-    assert np.array_equal(m_gpu, m_ref)                    # max is order independent
+    assert np.array_equal(m_gpu[:, 1], m_ref[:, 1])        # max|y_ref| exact
+    assert np.all(np.abs(m_gpu[:, 0] / m_ref[:, 0] - 1) <= RTOL_MAX)
     mae_g = s_gpu[:, 0] / s_gpu[:, 3]
     mae_r = s_ref[:, 0] / s_ref[:, 3]
-    assert np.all(np.abs(mae_g / mae_r - 1) < 1e-9)        # north star: 1%
-    assert np.all(np.abs(s_gpu[:, 1] / s_ref[:, 1] - 1) < 1e-9)
+    assert np.all(np.abs(mae_g / mae_r - 1) < RTOL_SUM)
+    assert np.all(np.abs(s_gpu[:, 1] / s_ref[:, 1] - 1) < RTOL_SUM)
     assert np.all(np.abs(s_gpu[:, 2] / s_ref[:, 2] - 1) < 1e-12)
 
 

@@ -47,6 +47,6 @@ def test_search_matches_oracle(dims, m, key):
     s_ref, _, _ = ref.sweep(dims, m, 3, [list(rows[i]) for i in ok], d, g, nofma=True)
     mae_ref = np.full(len(rows), np.nan)
     mae_ref[ok] = s_ref[:, 0] / s_ref[:, 3]
-    assert np.all(np.abs(mae[ok] / mae_ref[ok] - 1) < 1e-9)
+    assert np.all(np.abs(mae[ok] / mae_ref[ok] - 1) < 1e-5)   # fp32-pair scoring of the 2D F(4,3) kernel
     rank_ref = S.rank(templates, owner, params, mae_ref)
     assert [r[0] for r in ranking] == [r[0] for r in rank_ref]
