@@ -709,11 +709,13 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
 }
 
 // ------------------------------------------------------------------ K7 (1D)
+// Tile pairs in registers; scoring as in the register-resident 2D kernel: fp32 pairs
+// (Stat32) on y64 = hi + lo, exact fp64 careful path for non-finite outputs.
 template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
 __device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T (&d)[M + R - 1],
-                                       const typename Lane<PAIR, NOFMA>::T (&g)[R],
-                                       const double (&y64)[Lane<PAIR, NOFMA>::W][M], Stat& st, float* yd,
-                                       long long tile0, long long n_tiles, int tid) {
+                                       const typename Lane<PAIR, NOFMA>::T (&g)[R], const u64 (&yh)[M],
+                                       const u64 (&yl)[M], Stat& st, Stat32& st32, float* yd, long long tile0,
+                                       long long n_tiles, int tid) {
   using L = Lane<PAIR, NOFMA>;
   using T = typename L::T;
   constexpr int W = L::W;
@@ -737,18 +739,20 @@ __device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typen
 #pragma unroll
     for (int i = 0; i < N; i++)
       if (nz<ZA>(p * N + i)) y = L::fma(mw[i], cm[p * N + i], y);
+    if (DUMP) {
 #pragma unroll
-    for (int h = 0; h < W; h++) {
-      if (DUMP) {
+      for (int h = 0; h < W; h++) {
         const long long t = tile0 + tid + h * kSwThreads;
         if (t < n_tiles) yd[(tid + h * kSwThreads) * M + p] = L::get(y, h);
-      } else if (CAREFUL) {
-        if (h == 0) st.template add_careful<0>(L::get(y, h), y64[h][p]);
-        else st.template add_careful<1>(L::get(y, h), y64[h][p]);
-      } else {
-        if (h == 0) st.template add_fast<0>(L::get(y, h), y64[h][p]);
-        else st.template add_fast<1>(L::get(y, h), y64[h][p]);
       }
+    } else if (CAREFUL) {
+      float h0, h1, l0, l1;
+      Stat32::split(yh[p], h0, h1);
+      Stat32::split(yl[p], l0, l1);
+      st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
+      st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
+    } else {
+      st32.add(y, yh[p], yl[p]);
     }
   }
 }
@@ -763,6 +767,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
                                                              const __grid_constant__ IdxParam DI) {
   using L = Lane<PAIR, NOFMA>;
   using T = typename L::T;
+  static_assert(PAIR, "sweep1d_kernel evaluates tile pairs");
   constexpr int W = L::W;
   constexpr int N = M + R - 1;
   constexpr int PER = M * N + N * R + N * N;
@@ -785,7 +790,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
   const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
   for (int tb = tb_begin; tb < tb_end; tb++) {
     T d[kKP1][N], g[kKP1][R];
-    double y64[kKP1][W][M];
+    u64 yh[kKP1][M], yl[kKP1][M];   // y64 = hi + lo as fp32 pairs (tile A, tile B)
 #pragma unroll
     for (int k = 0; k < kKP1; k++) {
       const long long tk0 = (long long)tb * TPB + k * kSwThreads * W;  // tile0 of sub-block k
@@ -798,8 +803,19 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
         for (int j = 0; j < N; j++) dv[h][j] = ok ? __ldg(a.d + t * N + j) : 0.0f;
 #pragma unroll
         for (int j = 0; j < R; j++) gv[h][j] = ok ? __ldg(a.g + t * R + j) : 0.0f;
+      }
 #pragma unroll
-        for (int j = 0; j < M; j++) y64[k][h][j] = (ok && !DUMP) ? __ldg(a.y64 + t * M + j) : 0.0;
+      for (int j = 0; j < M; j++) {
+        float hi[2] = {0.0f, 0.0f}, lo[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int h = 0; h < W; h++) {
+          const long long t = tk0 + tid + h * kSwThreads;
+          const double v = (t < a.n_tiles && !DUMP) ? __ldg(a.y64 + t * M + j) : 0.0;
+          hi[h] = __double2float_rn(v);
+          lo[h] = __double2float_rn(v - (double)hi[h]);
+        }
+        yh[k][j] = Stat32::join(hi[0], hi[1]);
+        yl[k][j] = Stat32::join(lo[0], lo[1]);
       }
 #pragma unroll
       for (int j = 0; j < N; j++) {
@@ -815,26 +831,35 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
     for (int s = c_begin; s < c_end; s++) {
       const float* cm = P.v + s * PER;
       Stat st;
+      Stat32 st32;
 #pragma unroll
       for (int k = 0; k < kKP1; k++) {
         const long long tk0 = (long long)tb * TPB + k * kSwThreads * W;
         float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tk0) * M : nullptr;
-        eval1d<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d[k], g[k], y64[k], st, yd, tk0, a.n_tiles, tid);
+        eval1d<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d[k], g[k], yh[k], yl[k], st, st32, yd, tk0,
+                                                           a.n_tiles, tid);
       }
       if (!DUMP) {
-        if (__any_sync(0xffffffffu, !st.finite())) {
-          st = Stat();
+        double r0, r1, rm, rn = 0.0;
+        if (__any_sync(0xffffffffu, !st32.finite())) {
 #pragma unroll
           for (int k = 0; k < kKP1; k++)
-            eval1d<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d[k], g[k], y64[k], st, nullptr, 0, a.n_tiles, tid);
+            eval1d<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d[k], g[k], yh[k], yl[k], st, st32, nullptr, 0,
+                                                               a.n_tiles, tid);
+          st.warp_reduce();
+          r0 = st.s0[0];
+          r1 = st.s1[0];
+          rm = st.m0[0];
+          rn = (double)st.nonfin;
+        } else {
+          st32.warp_reduce(r0, r1, rm);
         }
-        st.warp_reduce();
         if (lane == 0) {
           double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
-          acc[0] += st.s0[0];
-          acc[1] += st.s1[0];
-          acc[2] = st.m0[0] > acc[2] ? st.m0[0] : acc[2];
-          acc[3] += (double)st.nonfin;
+          acc[0] += r0;
+          acc[1] += r1;
+          acc[2] = rm > acc[2] ? rm : acc[2];
+          acc[3] += rn;
         }
       }
     }
