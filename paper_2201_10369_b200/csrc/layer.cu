@@ -13,6 +13,7 @@
 // the sign of a zero).  Parity semantics: every dot product is an
 // fmaf chain from +0 in ascending index order, 2D transforms left product first.
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 
 #include "wino_internal.h"
@@ -405,23 +406,34 @@ __global__ void score_finalize_kernel(const double* __restrict__ partial, int n_
 // ------------------------------------------------------------------ K9 ReLU (+ 2x2/2 max pool)
 // Network glue of BASELINE.json configs[4] (VGG-16: "ReLU + 2x2 maxpool").  Both are exact
 // operations (max, and the sign test), so they add no rounding.  pool = 1: ReLU only.
-__global__ void relu_pool_kernel(const float* __restrict__ x, float* __restrict__ y, long long NC, int H, int W,
-                                 int pool) {
-  // grid.x covers one (n, c) plane's outputs, grid.y strides over the planes: 32-bit
-  // in-plane index math, coalesced rows
-  const int Ho = H / pool, Wo = W / pool;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= Ho * Wo) return;
-  const int h = o / Wo, w = o - h * Wo;
-  for (long long nc = blockIdx.y; nc < NC; nc += gridDim.y) {
-    const float* src = x + nc * H * W + (h * pool) * W + w * pool;
-    float v = 0.0f;   // ReLU: max(0, ·)
-    if (pool == 2) {
-      v = fmaxf(fmaxf(v, fmaxf(__ldg(src), __ldg(src + 1))), fmaxf(__ldg(src + W), __ldg(src + W + 1)));
-    } else {
-      v = fmaxf(v, __ldg(src));
-    }
-    y[nc * Ho * Wo + o] = v;
+// pool = 1: flat ReLU, float4 grid-stride; pool = 2: one warp per output row (n, c, h),
+// index arithmetic once per row, lanes over the row's columns (float2 loads of the two
+// input rows).
+__global__ void relu_kernel(const float4* __restrict__ x, float4* __restrict__ y, long long n4) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    y[i] = make_float4(fmaxf(v.x, 0.0f), fmaxf(v.y, 0.0f), fmaxf(v.z, 0.0f), fmaxf(v.w, 0.0f));
+  }
+}
+
+__global__ void relu_pool1_scalar_kernel(const float* __restrict__ x, float* __restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = fmaxf(__ldg(x + i), 0.0f);
+}
+
+__global__ void relu_pool2_kernel(const float* __restrict__ x, float* __restrict__ y, long long rows, int H, int W) {
+  const int Ho = H / 2, Wo = W / 2;
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const long long nc = row / Ho;
+  const int h = (int)(row - nc * Ho);
+  const float* r0 = x + (nc * H + 2 * h) * W;
+  const float* r1 = r0 + W;
+  float* dst = y + row * Wo;
+  for (int w = threadIdx.x & 31; w < Wo; w += 32) {
+    const float a = fmaxf(__ldg(r0 + 2 * w), __ldg(r0 + 2 * w + 1));
+    const float b = fmaxf(__ldg(r1 + 2 * w), __ldg(r1 + 2 * w + 1));
+    dst[w] = fmaxf(fmaxf(a, b), 0.0f);   // ReLU then max == max then ReLU (monotone)
   }
 }
 
@@ -480,14 +492,27 @@ WsLayout ws_layout(const Geo& g) {
 
 int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int pool, cudaStream_t stream) {
   const long long total = (long long)N * C * (H / pool) * (W / pool);
-  const int threads = 256;
-  const dim3 grid((unsigned)(((H / pool) * (W / pool) + threads - 1) / threads),
-                  (unsigned)std::min<long long>((long long)N * C, 65535));
-  if (total > 0)
-    timed_launch("relu_pool", stream, [&] {
-      relu_pool_kernel<<<grid, threads, 0, stream>>>(x, y, (long long)N * C, H, W, pool);
-    });
-  count_launches(total > 0 ? 1 : 0);
+  int launches = 0;
+  if (total > 0) {
+    if (pool == 1 && total % 4 == 0 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0) {
+      timed_launch("relu_pool", stream, [&] {
+        relu_kernel<<<148 * 16, 256, 0, stream>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+                                                  total / 4);
+      });
+    } else if (pool == 1) {
+      // unaligned or ragged: treat as pool-1 rows through the row kernel's scalar path
+      timed_launch("relu_pool", stream, [&] {
+        relu_pool1_scalar_kernel<<<148 * 16, 256, 0, stream>>>(x, y, total);
+      });
+    } else {
+      const long long rows = (long long)N * C * (H / 2);
+      timed_launch("relu_pool", stream, [&] {
+        relu_pool2_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, stream>>>(x, y, rows, H, W);
+      });
+    }
+    launches = 1;
+  }
+  count_launches(launches);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(WINO_E_CUDA, "relu_pool launch: %s", cudaGetErrorString(e));
   return WINO_OK;
