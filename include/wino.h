@@ -100,6 +100,17 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y,
                      const double* points, void* workspace, size_t workspace_bytes,
                      double* d_sums, double* d_maxs, void* stream);
 
+/* (2c) wino_conv2d_fp32 with variant flags (NEXT row N3, reported separately):
+ *   WINO_CONV_TF32: the channel contraction runs on the 5th-generation tensor cores
+ *   (tcgen05.mma kind::tf32, accumulator in tensor memory).  TF32 keeps 10 mantissa bits of
+ *   each operand, so this variant does NOT have the parity semantics above; its error is
+ *   what the scored statistics measure.  Same arguments and workspace as (2). */
+#define WINO_CONV_TF32 1u
+int wino_conv2d_fp32_ex(const float* x, const float* w, float* y,
+                        int N, int C, int H, int W, int K, int r, int pad, int m,
+                        const double* points, void* workspace, size_t workspace_bytes,
+                        double* d_sums, double* d_maxs, unsigned flags, void* stream);
+
 /* (2b) Network glue for BASELINE.json configs[4] (VGG-16 "ReLU + 2x2 maxpool"):
  *   y[n][c][h][w] = max(0, max_{a,b < pool} x[n][c][pool h + a][pool w + b]), pool 1 | 2
  *   (2 x 2 window, stride 2, floor).  x: DEVICE float[N][C][H][W], y: DEVICE
@@ -137,7 +148,7 @@ int wino_last_launch_count(void);
 /* Kernel timing hook (profiling / bench.py roofline).  While enabled, every launch is
  * bracketed by two cudaEvents recorded on its own stream and filed under its kernel
  * family: "sweep1d", "sweep2d", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
- * "layer_filter", "layer_input", "layer_gemm", "layer_output", "layer_score",
+ * "layer_filter", "layer_input", "layer_gemm", "layer_gemm_tf32", "layer_output", "layer_score",
  * "layer_score_finalize", "relu_pool".  wino_timing_read() synchronises on the recorded events and
  * returns the summed milliseconds and launch count of one family since the last reset.
  * Returns the previous enable state / a wino_status. */

@@ -15,6 +15,7 @@ from ._lib import check, load
 WINO_SUMS = 5
 WINO_MAXS = 2
 WINO_SWEEP_NOFMA = 1
+WINO_CONV_TF32 = 1
 WINO_MAX_N = 16
 
 _d = ctypes.POINTER(ctypes.c_double)
@@ -65,18 +66,23 @@ def wino_conv2d_workspace_bytes(N, C, H, W, K, r, pad, m) -> int:
 
 
 def wino_conv2d_fp32(x, w, y, pad: int, m: int, points: Sequence[float], workspace,
-                     d_sums=None, d_maxs=None, stream=None) -> None:
+                     d_sums=None, d_maxs=None, stream=None, flags: int = 0) -> None:
     """x [N,C,H,W], w [K,C,r,r], y [N,K,Ho,Wo] fp32 CUDA tensors; workspace uint8 CUDA
-    tensor; d_sums [5] / d_maxs [2] fp64 CUDA tensors (accumulated) or None."""
+    tensor; d_sums [5] / d_maxs [2] fp64 CUDA tensors (accumulated) or None.  flags != 0
+    calls wino_conv2d_fp32_ex (WINO_CONV_TF32: the tensor-core variant)."""
     N, C, H, W = x.shape
     K, C2, r, r2 = w.shape
     if C2 != C or r2 != r:
         raise ValueError("weight shape mismatch")
     pts = _np64(points)
-    st = load().wino_conv2d_fp32(_ptr(x), _ptr(w), _ptr(y), N, C, H, W, K, r, pad, m, pts.ctypes.data_as(_d),
-                                 _ptr(workspace), workspace.numel() * workspace.element_size(),
-                                 _ptr(d_sums), _ptr(d_maxs), _stream_ptr(stream))
-    check(st, "wino_conv2d_fp32")
+    args = (_ptr(x), _ptr(w), _ptr(y), N, C, H, W, K, r, pad, m, pts.ctypes.data_as(_d),
+            _ptr(workspace), workspace.numel() * workspace.element_size(), _ptr(d_sums), _ptr(d_maxs))
+    if flags:
+        st = load().wino_conv2d_fp32_ex(*args, flags, _stream_ptr(stream))
+        check(st, "wino_conv2d_fp32_ex")
+    else:
+        st = load().wino_conv2d_fp32(*args, _stream_ptr(stream))
+        check(st, "wino_conv2d_fp32")
 
 
 def wino_relu_pool_fp32(x, y, pool: int, stream=None) -> None:
@@ -141,7 +147,7 @@ def wino_timing_read(family: str) -> Tuple[float, int]:
 
 # ------------------------------------------------------------------ convenience (still marshalling only)
 
-def conv2d(x, w, pad: int, m: int, points, score: bool = False, stream=None):
+def conv2d(x, w, pad: int, m: int, points, score: bool = False, stream=None, flags: int = 0):
     """Allocate y / workspace with torch and run wino_conv2d_fp32.  Returns (y, sums, maxs)."""
     import torch
     N, C, H, W = x.shape
@@ -153,5 +159,5 @@ def conv2d(x, w, pad: int, m: int, points, score: bool = False, stream=None):
     if score:
         sums = torch.zeros(WINO_SUMS, dtype=torch.float64, device=x.device)
         maxs = torch.zeros(WINO_MAXS, dtype=torch.float64, device=x.device)
-    wino_conv2d_fp32(x, w, y, pad, m, points, ws, sums, maxs, stream)
+    wino_conv2d_fp32(x, w, y, pad, m, points, ws, sums, maxs, stream, flags)
     return y, sums, maxs

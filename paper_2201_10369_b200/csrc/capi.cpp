@@ -148,10 +148,18 @@ size_t wino_conv2d_workspace_bytes(int N, int C, int H, int W, int K, int r, int
 int wino_conv2d_fp32(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
                      int m, const double* points, void* workspace, size_t workspace_bytes, double* d_sums,
                      double* d_maxs, void* stream) {
+  return wino_conv2d_fp32_ex(x, w, y, N, C, H, W, K, r, pad, m, points, workspace, workspace_bytes, d_sums, d_maxs,
+                             0u, stream);
+}
+
+int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
+                        int m, const double* points, void* workspace, size_t workspace_bytes, double* d_sums,
+                        double* d_maxs, unsigned flags, void* stream) {
   reset_launches();
   if (!x || !w || !y || !points) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || r < 1 || m < 1 || pad < 0)
     return set_error(WINO_E_INVALID_ARG, "non-positive size or negative pad");
+  if (flags & ~WINO_CONV_TF32) return set_error(WINO_E_INVALID_ARG, "unknown flags");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
   if (H + 2 * pad < r || W + 2 * pad < r) return set_error(WINO_E_BAD_SHAPE, "empty output");
@@ -166,7 +174,7 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y, int N, int C, int
   to_f32(G.data(), n * r, Gf.data());
   to_f32(BT.data(), n * n, BTf.data());
   return finish(layer_launch(x, w, y, N, C, H, W, K, r, pad, m, ATf.data(), Gf.data(), BTf.data(), workspace,
-                             workspace_bytes, d_sums, d_maxs, (cudaStream_t)stream));
+                             workspace_bytes, d_sums, d_maxs, flags, (cudaStream_t)stream));
 }
 
 int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, int pool, void* stream) {

@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstdio>
 
+#include "tc_gemm.cuh"
 #include "wino_internal.h"
 
 namespace wino {
@@ -38,9 +39,18 @@ struct Geo {
   long long T;     // tiles = N * th * tw
   int Cp, Kp;
   long long Tp;
+  int tf32;        // 1: U / V are rounded to TF32 (nearest, ties away) for the tcgen05 variant
 };
 
-Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m) {
+// round-to-nearest fp32 -> TF32 (10 explicit mantissa bits); the tensor core would otherwise
+// drop the low 13 bits (measured: truncation)
+__device__ __forceinline__ float round_tf32(float v) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+
+Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, bool tf32 = false) {
   Geo g;
   g.N = N; g.C = C; g.H = H; g.W = W; g.K = K; g.r = r; g.pad = pad; g.m = m;
   g.Ho = H + 2 * pad - r + 1;
@@ -48,16 +58,19 @@ Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m) {
   g.th = (g.Ho + m - 1) / m;
   g.tw = (g.Wo + m - 1) / m;
   g.T = (long long)N * g.th * g.tw;
-  g.Cp = (C + 15) / 16 * 16;
+  // FFMA GEMM: BK = 16, BN = 128; tcgen05 variant: BK = 32, N = 256
+  const int ca = tf32 ? 32 : 16, ta = tf32 ? 256 : 128;
+  g.Cp = (C + ca - 1) / ca * ca;
   g.Kp = (K + 127) / 128 * 128;
-  g.Tp = (g.T + 127) / 128 * 128;
+  g.Tp = (g.T + ta - 1) / ta * ta;
+  g.tf32 = tf32 ? 1 : 0;
   return g;
 }
 
 
 // ------------------------------------------------------------------ K1
 template <int M, int R>
-__global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U, int C, int K, int Cp, int Kp,
+__global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U, int C, int K, int Cp, int Kp, int tf32,
                               const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp * Kp, k fastest
@@ -90,7 +103,7 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
       float acc = 0.0f;
 #pragma unroll
       for (int q = 0; q < R; q++) acc = __fmaf_rn(t1[i][q], mt.G[l * R + q], acc);
-      U[(i * N + l) * plane + idx] = acc;
+      U[(i * N + l) * plane + idx] = tf32 ? round_tf32(acc) : acc;
     }
 }
 
@@ -143,7 +156,7 @@ __global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V,
       float acc = 0.0f;
 #pragma unroll
       for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
-      V[(i * N + l) * plane + idx] = acc;
+      V[(i * N + l) * plane + idx] = geo.tf32 ? round_tf32(acc) : acc;
     }
 }
 
@@ -234,6 +247,10 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
     *reinterpret_cast<ulonglong2*>(row + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
   }
 }
+
+// ------------------------------------------------------------------ K3 variant (NEXT row N3)
+// tcgen05 kind::tf32 contraction: tc::gemm_tf32_kernel in tc_gemm.cuh.  NOT the parity path.
+using tc::gemm_tf32_kernel;
 
 // ------------------------------------------------------------------ K4
 // one thread per (k, t); t fastest -> coalesced M loads per Winograd position
@@ -438,7 +455,7 @@ __global__ void relu_pool2_kernel(const float* __restrict__ x, float* __restrict
 }
 
 // ------------------------------------------------------------------ dispatch
-typedef void (*FilterK)(const float*, float*, int, int, int, int, LayerMats);
+typedef void (*FilterK)(const float*, float*, int, int, int, int, int, LayerMats);
 typedef void (*InputK)(const float*, float*, Geo, LayerMats);
 typedef void (*OutputK)(const float*, float*, Geo, LayerMats);
 typedef void (*ScoreK)(const float*, const float*, const float*, Geo, double*);
@@ -521,15 +538,18 @@ int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int p
 int layer_supported(int m, int r) { return find_layer(m, r) != nullptr; }
 
 size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m) {
-  return ws_layout(make_geo(N, C, H, W, K, r, pad, m)).total;
+  // large enough for the FFMA path and the tcgen05 variant's alignments
+  return std::max(ws_layout(make_geo(N, C, H, W, K, r, pad, m, false)).total,
+                  ws_layout(make_geo(N, C, H, W, K, r, pad, m, true)).total);
 }
 
 int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
                  int m, const float* AT, const float* G, const float* BT, void* workspace, size_t ws_bytes,
-                 double* d_sums, double* d_maxs, cudaStream_t stream) {
+                 double* d_sums, double* d_maxs, unsigned flags, cudaStream_t stream) {
   const LayerCfg* cfg = find_layer(m, r);
   if (!cfg) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
-  const Geo g = make_geo(N, C, H, W, K, r, pad, m);
+  const bool tf32 = (flags & WINO_CONV_TF32) != 0;
+  const Geo g = make_geo(N, C, H, W, K, r, pad, m, tf32);
   const WsLayout L = ws_layout(g);
   if (!workspace || ws_bytes < L.total)
     return set_error(WINO_E_WORKSPACE, "layer workspace %zu < %zu bytes", ws_bytes, L.total);
@@ -552,7 +572,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     const long long tot = (long long)g.Cp * g.Kp;
     const auto fk = cfg->fk;
     timed_launch("layer_filter", stream,
-                 [&] { fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(w, U, C, K, g.Cp, g.Kp, mt); });
+                 [&] { fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(w, U, C, K, g.Cp, g.Kp, g.tf32, mt); });
     launches++;
   }
   {
@@ -562,14 +582,25 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     launches++;
   }
   {
-    dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute((const void*)gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      attr = true;
+    if (tf32) {
+      static bool tattr = false;
+      if (!tattr) {
+        cudaFuncSetAttribute((const void*)gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmem);
+        tattr = true;
+      }
+      dim3 grid((unsigned)(g.Tp / tc::kN), (unsigned)(g.Kp / tc::kM), (unsigned)(n * n));
+      timed_launch("layer_gemm_tf32", stream,
+                   [&] { gemm_tf32_kernel<<<grid, tc::kThreads, tc::kSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
+    } else {
+      dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute((const void*)gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+        attr = true;
+      }
+      timed_launch("layer_gemm", stream,
+                   [&] { gemm_kernel<<<grid, 256, kGemmSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
     }
-    timed_launch("layer_gemm", stream,
-                 [&] { gemm_kernel<<<grid, 256, kGemmSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
     launches++;
   }
   {
