@@ -227,7 +227,25 @@ def bench_layer(torch, dev, flush, steps=10):
         b.record(stream)
         b.synchronize()
         sc.append(a.elapsed_time(b))
+    # NEXT row N3: the tcgen05 kind::tf32 contraction variant (not the parity path)
+    tf = []
+    api.wino_timing_reset()
+    for _ in range(steps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, flags=api.WINO_CONV_TF32)
+        b.record(stream)
+        b.synchronize()
+        tf.append(a.elapsed_time(b))
+    kern_tf = {f: api.wino_timing_read(f)[0] / steps
+               for f in ["layer_filter", "layer_input", "layer_gemm_tf32", "layer_output"]}
+    sums_tf = torch.zeros(5, dtype=torch.float64, device=dev)
+    maxs_tf = torch.zeros(2, dtype=torch.float64, device=dev)
+    api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sums_tf, maxs_tf, flags=api.WINO_CONV_TF32)
+    torch.cuda.synchronize()
     api.wino_timing_enable(False)
+    s_tf = sums_tf.cpu().numpy()
     s = sums.cpu().numpy() / 2
     t = statistics.median(ts)
     direct_flop = 2.0 * N * K * C * Ho * Wo * r * r
@@ -241,12 +259,29 @@ def bench_layer(torch, dev, flush, steps=10):
     tr_fma = K * C * (r + n) * nzG + C * T * 2 * n * nzB + K * T * (n + m) * nzA
     f_alg = 2.0 * (gemm_mac + tr_fma)
     b_alg = 4.0 * (x.size + w.size + N * K * Ho * Wo)
+    # tf32 GEMM kernel: algorithmic HBM bytes = read U and V once, write M once (padded sizes)
+    Cp, Kp, Tp = -(-C // 32) * 32, -(-K // 128) * 128, -(-T // 256) * 256
+    gemm_bytes = 4.0 * n * n * (Cp * Kp + Cp * Tp + Kp * Tp)
+    g_ms = kern_tf["layer_gemm_tf32"]
+    peaks, psrc = _peaks()
+    t_tf = statistics.median(tf)
+    tf32 = {
+        "ms": t_tf, "effective_tflops": direct_flop / (t_tf * 1e-3) / 1e12, "kernel_ms": kern_tf,
+        "gemm_tflops": 2.0 * gemm_mac / (g_ms * 1e-3) / 1e12 if g_ms else None,
+        "gemm_roofline": {"bound": "hbm", "achieved_gbs": gemm_bytes / (g_ms * 1e-3) / 1e9 if g_ms else None,
+                          "peak_gbs": peaks["hbm_gbs"], "peak_source": psrc,
+                          "frac": gemm_bytes / (g_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] if g_ms else None},
+        "scored_mae": float(s_tf[0] / s_tf[3]) if s_tf[3] else None,
+        "note": "WINO_CONV_TF32: tcgen05.mma kind::tf32 (TMA-fed, TMEM accumulators); operands rounded to "
+                "TF32, so NOT the fp32 parity path -- reported separately",
+    }
     return {
         "workload": "configs[2] F(6x6,3x3) N=32 C=K=256 56x56 pad 1, points {0,±2,±1/2,-1/1.003,1.003,inf}",
         "ms": t, "ms_min": min(ts), "effective_tflops": direct_flop / (t * 1e-3) / 1e12,
         "kernel_ms": kern, "flop_alg": f_alg, "bytes_alg": b_alg,
         "scored_ms": statistics.median(sc), "scored_mae": float(s[0] / s[3]) if s[3] else None,
         "l2": "flushed (512 MB write) before every run",
+        "tf32_variant": tf32,
     }, f_alg, b_alg, t
 
 

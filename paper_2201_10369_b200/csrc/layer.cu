@@ -588,9 +588,23 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
         cudaFuncSetAttribute((const void*)gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmem);
         tattr = true;
       }
-      dim3 grid((unsigned)(g.Tp / tc::kN), (unsigned)(g.Kp / tc::kM), (unsigned)(n * n));
-      timed_launch("layer_gemm_tf32", stream,
-                   [&] { gemm_tf32_kernel<<<grid, tc::kThreads, tc::kSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
+      static int n_sm = 0;
+      if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      }
+      const long long tiles = (long long)(n * n) * (g.Kp / tc::kM) * (g.Tp / tc::kN);
+      const unsigned grid = (unsigned)std::min<long long>(tiles, n_sm);
+      CUtensorMap tmU, tmV, tmM;
+      const unsigned long long pc = (unsigned long long)(n * n) * g.Cp, pk = (unsigned long long)(n * n) * g.Kp;
+      if (!tc::encode_map_2d(&tmU, U, (unsigned long long)g.Kp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+          !tc::encode_map_2d(&tmV, V, (unsigned long long)g.Tp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+          !tc::encode_map_2d(&tmM, Mw, (unsigned long long)g.Tp, pk, CU_TENSOR_MAP_SWIZZLE_128B))
+        return set_error(WINO_E_CUDA, "cuTensorMapEncodeTiled failed for the tf32 contraction");
+      timed_launch("layer_gemm_tf32", stream, [&] {
+        gemm_tf32_kernel<<<grid, tc::kThreads, tc::kSmem, stream>>>(tmU, tmV, tmM, g.Cp, g.Kp, g.Tp, n * n);
+      });
     } else {
       dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
       static bool attr = false;

@@ -22,12 +22,30 @@ int main(int argc, char** argv) {
   cudaMemcpy(dV, V.data(), V.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(dM, 0xff, M.size() * 4);
   cudaFuncSetAttribute((const void*)wino::tc::gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::kSmem);
-  dim3 grid((unsigned)(Tp / wino::tc::kN), (unsigned)(Kp / wino::tc::kM), 1);
-  wino::tc::gemm_tf32_kernel<<<grid, wino::tc::kThreads, wino::tc::kSmem>>>(dU, dV, dM, Cp, Kp, Tp);
+  const int grid = argc > 5 ? atoi(argv[5]) : 148;   // persistent CTAs (fewer -> several tiles each)
+  CUtensorMap tmU, tmV, tmM;
+  const char* sw = getenv("TC_SWZ");
+  const CUtensorMapSwizzle swz = (!sw || !*sw) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                     : (atoi(sw) == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!wino::tc::encode_map_2d(&tmU, dU, Kp, Cp, swz) || !wino::tc::encode_map_2d(&tmV, dV, Tp, Cp, swz) ||
+      !wino::tc::encode_map_2d(&tmM, dM, Tp, Kp, CU_TENSOR_MAP_SWIZZLE_128B)) {
+    printf("encode failed\n");
+    return 2;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int rep = 0; rep < 4; rep++) {
+    cudaEventRecord(e0);
+    wino::tc::gemm_tf32_kernel<<<grid, wino::tc::kThreads, wino::tc::kSmem>>>(tmU, tmV, tmM, Cp, Kp, Tp, 1);
+    cudaEventRecord(e1);
+  }
   cudaError_t e = cudaDeviceSynchronize();
-  printf("kernel: %s\n", cudaGetErrorString(e));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("kernel: %s  %.3f ms\n", cudaGetErrorString(e), ms);
   cudaMemcpy(M.data(), dM, M.size() * 4, cudaMemcpyDeviceToHost);
   long long bad = 0, nan = 0, zero = 0;
+  if (getenv("TC_NOCHECK")) return 0;
   for (int k = 0; k < Kp; k++)
     for (long long t = 0; t < Tp; t++) {
       double ref = 0;
