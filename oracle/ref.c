@@ -6,6 +6,9 @@
  *                                          2D  Y = Aᵀ[(GgGᵀ) ⊙ (BᵀdB)]A    (eq:conv_2d P:181)
  *     every dot product is  acc = +0; for j ascending: acc = fmaf(a_j, b_j, acc)      (O5)
  *     or, in the paper-arithmetic mode, acc = RN(acc + RN(a_j*b_j))               (O6)
+ *     or, in the Huffman mode (mode 2, "Huffman tree evaluation order"), the
+ *     products RN(a_j*b_j) of the non-zero matrix coefficients summed along a Huffman
+ *     tree over the coefficient magnitudes |a_j| (reading R21);
  *     2D passes: left product first, then right (reading R8);
  *   - fp64 direct valid cross-correlation of the same fp32 data (eq:conv P:112; O7);
  *   - error statistics of y32 against y64 ("L1 norm ... normal convolution using
@@ -32,6 +35,56 @@ static inline float mac(float acc, float a, float b, int nofma) {
   return fmaf(a, b, acc);
 }
 
+/* Huffman-order dot product (mode 2): leaves are the terms with a non-zero matrix
+ * coefficient, p_j = RN(coef_j * x_j) with weight |coef_j| (fp64); repeatedly the two
+ * alive nodes of smallest (weight, seq) are replaced by RN(v_a + v_b) with weight
+ * w_a + w_b (fp64) and seq = len + k (leaves have seq = j), i.e. ties go to leaves in
+ * index order, then to older internal nodes.  No terms -> +0. */
+static float dot_huffman(const float* coef, int cs, const float* x, int xs, int len) {
+  float v[2 * OMAXN];
+  double w[2 * OMAXN];
+  int seq[2 * OMAXN], alive[2 * OMAXN];
+  int cnt = 0;
+  for (int j = 0; j < len; j++) {
+    const float c = coef[j * cs];
+    if (c == 0.0f) continue;
+    v[cnt] = c * x[j * xs];
+    w[cnt] = fabs((double)c);
+    seq[cnt] = j;
+    alive[cnt] = 1;
+    cnt++;
+  }
+  if (cnt == 0) return 0.0f;
+  const int leaves = cnt;
+  for (int k = 0; k < leaves - 1; k++) {
+    int pick[2];
+    for (int t = 0; t < 2; t++) {
+      int best = -1;
+      for (int i = 0; i < cnt; i++) {
+        if (!alive[i]) continue;
+        if (best < 0 || w[i] < w[best] || (w[i] == w[best] && seq[i] < seq[best])) best = i;
+      }
+      alive[best] = 0;
+      pick[t] = best;
+    }
+    v[cnt] = v[pick[0]] + v[pick[1]];
+    w[cnt] = w[pick[0]] + w[pick[1]];
+    seq[cnt] = len + k;
+    alive[cnt] = 1;
+    cnt++;
+  }
+  return v[cnt - 1];
+}
+
+/* dot product of a coefficient row (stride cs) with data x (stride xs) in `mode`
+ * (0: fmaf chain, 1: RN(acc + RN(a*b)) chain, 2: Huffman order). */
+static inline float dot(const float* coef, int cs, const float* x, int xs, int len, int mode) {
+  if (mode == 2) return dot_huffman(coef, cs, x, xs, len);
+  float acc = 0.0f;
+  for (int j = 0; j < len; j++) acc = mac(acc, coef[j * cs], x[j * xs], mode);
+  return acc;
+}
+
 /* ---------------------------------------------------------------- one tile */
 
 /* 1D: U = G g, V = Bᵀ d, M = U ⊙ V, y = Aᵀ M.  AT[m][n], G[n][r], BT[n][n] row-major. */
@@ -39,73 +92,37 @@ static void tile_1d(int m, int r, const float* AT, const float* G, const float* 
                     const float* d, const float* g, int nofma, float* y) {
   const int n = m + r - 1;
   float U[OMAXN], V[OMAXN], M[OMAXN];
-  for (int i = 0; i < n; i++) {
-    float acc = 0.0f;
-    for (int j = 0; j < r; j++) acc = mac(acc, G[i * r + j], g[j], nofma);
-    U[i] = acc;
-  }
-  for (int i = 0; i < n; i++) {
-    float acc = 0.0f;
-    for (int j = 0; j < n; j++) acc = mac(acc, BT[i * n + j], d[j], nofma);
-    V[i] = acc;
-  }
-  for (int i = 0; i < n; i++) M[i] = mac(0.0f, U[i], V[i], nofma);
-  for (int p = 0; p < m; p++) {
-    float acc = 0.0f;
-    for (int i = 0; i < n; i++) acc = mac(acc, AT[p * n + i], M[i], nofma);
-    y[p] = acc;
-  }
+  for (int i = 0; i < n; i++) U[i] = dot(G + i * r, 1, g, 1, r, nofma);
+  for (int i = 0; i < n; i++) V[i] = dot(BT + i * n, 1, d, 1, n, nofma);
+  for (int i = 0; i < n; i++) M[i] = mac(0.0f, U[i], V[i], nofma != 0);
+  for (int p = 0; p < m; p++) y[p] = dot(AT + p * n, 1, M, 1, n, nofma);
 }
 
 /* 2D filter transform U = G g Gᵀ:  T1[i][q] = Σ_j G[i][j] g[j][q];  U[i][l] = Σ_q T1[i][q] G[l][q]. */
 static void filter_2d(int n, int r, const float* G, const float* g, int nofma, float* U) {
   float T1[OMAXN * OMAXN];
   for (int i = 0; i < n; i++)
-    for (int q = 0; q < r; q++) {
-      float acc = 0.0f;
-      for (int j = 0; j < r; j++) acc = mac(acc, G[i * r + j], g[j * r + q], nofma);
-      T1[i * r + q] = acc;
-    }
+    for (int q = 0; q < r; q++) T1[i * r + q] = dot(G + i * r, 1, g + q, r, r, nofma);
   for (int i = 0; i < n; i++)
-    for (int l = 0; l < n; l++) {
-      float acc = 0.0f;
-      for (int q = 0; q < r; q++) acc = mac(acc, T1[i * r + q], G[l * r + q], nofma);
-      U[i * n + l] = acc;
-    }
+    for (int l = 0; l < n; l++) U[i * n + l] = dot(G + l * r, 1, T1 + i * r, 1, r, nofma);
 }
 
 /* 2D input transform V = Bᵀ d B:  T2[i][q] = Σ_j BT[i][j] d[j][q];  V[i][l] = Σ_q T2[i][q] BT[l][q]. */
 static void input_2d(int n, const float* BT, const float* d, int nofma, float* V) {
   float T2[OMAXN * OMAXN];
   for (int i = 0; i < n; i++)
-    for (int q = 0; q < n; q++) {
-      float acc = 0.0f;
-      for (int j = 0; j < n; j++) acc = mac(acc, BT[i * n + j], d[j * n + q], nofma);
-      T2[i * n + q] = acc;
-    }
+    for (int q = 0; q < n; q++) T2[i * n + q] = dot(BT + i * n, 1, d + q, n, n, nofma);
   for (int i = 0; i < n; i++)
-    for (int l = 0; l < n; l++) {
-      float acc = 0.0f;
-      for (int q = 0; q < n; q++) acc = mac(acc, T2[i * n + q], BT[l * n + q], nofma);
-      V[i * n + l] = acc;
-    }
+    for (int l = 0; l < n; l++) V[i * n + l] = dot(BT + l * n, 1, T2 + i * n, 1, n, nofma);
 }
 
 /* 2D output transform Y = Aᵀ Mw A:  T3[p][l] = Σ_i AT[p][i] Mw[i][l];  Y[p][s] = Σ_l T3[p][l] AT[s][l]. */
 static void output_2d(int m, int n, const float* AT, const float* Mw, int nofma, float* Y) {
   float T3[OMAXN * OMAXN];
   for (int p = 0; p < m; p++)
-    for (int l = 0; l < n; l++) {
-      float acc = 0.0f;
-      for (int i = 0; i < n; i++) acc = mac(acc, AT[p * n + i], Mw[i * n + l], nofma);
-      T3[p * n + l] = acc;
-    }
+    for (int l = 0; l < n; l++) T3[p * n + l] = dot(AT + p * n, 1, Mw + l, n, n, nofma);
   for (int p = 0; p < m; p++)
-    for (int s = 0; s < m; s++) {
-      float acc = 0.0f;
-      for (int l = 0; l < n; l++) acc = mac(acc, T3[p * n + l], AT[s * n + l], nofma);
-      Y[p * m + s] = acc;
-    }
+    for (int s = 0; s < m; s++) Y[p * m + s] = dot(AT + s * n, 1, T3 + p * n, 1, n, nofma);
 }
 
 static void tile_2d(int m, int r, const float* AT, const float* G, const float* BT,
@@ -114,7 +131,7 @@ static void tile_2d(int m, int r, const float* AT, const float* G, const float* 
   float U[OMAXN * OMAXN], V[OMAXN * OMAXN], Mw[OMAXN * OMAXN];
   filter_2d(n, r, G, g, nofma, U);
   input_2d(n, BT, d, nofma, V);
-  for (int i = 0; i < n * n; i++) Mw[i] = mac(0.0f, U[i], V[i], nofma);
+  for (int i = 0; i < n * n; i++) Mw[i] = mac(0.0f, U[i], V[i], nofma != 0);
   output_2d(m, n, AT, Mw, nofma, y);
 }
 

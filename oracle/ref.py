@@ -74,11 +74,17 @@ def pack_mats(m: int, r: int, point_sets: Sequence[Sequence[float]]) -> np.ndarr
     return np.ascontiguousarray(np.stack(rows), dtype=np.float32)
 
 
-def tile(dims, m, r, AT, G, BT, d, g, nofma=False) -> np.ndarray:
+def _mode(nofma, huffman):
+    """0: F32-FMA chains, 1: F32-NOFMA chains, 2: Huffman order (NOFMA products)."""
+    return 2 if huffman else int(bool(nofma))
+
+
+def tile(dims, m, r, AT, G, BT, d, g, nofma=False, huffman=False) -> np.ndarray:
     y = np.zeros(m ** dims, dtype=np.float32)
     AT, G, BT, d, g = map(_c32, (AT, G, BT, d, g))
     rc = lib().oref_tile(dims, m, r, _p(AT, ctypes.c_float), _p(G, ctypes.c_float), _p(BT, ctypes.c_float),
-                         _p(d, ctypes.c_float), _p(g, ctypes.c_float), int(nofma), _p(y, ctypes.c_float))
+                         _p(d, ctypes.c_float), _p(g, ctypes.c_float), _mode(nofma, huffman),
+                         _p(y, ctypes.c_float))
     if rc:
         raise ValueError("oref_tile failed")
     return y
@@ -93,11 +99,12 @@ def direct64_tiles(dims, m, r, d_tiles, g_tiles) -> np.ndarray:
     return y
 
 
-def sweep(dims, m, r, point_sets, d_tiles, g_tiles, nofma=False, n_dump=0, mats=None):
-    """O9.  Returns (sums [S,5], maxs [S,2], y_dump [S,n_dump,m^dims] or None)."""
+def sweep(dims, m, r, point_sets, d_tiles, g_tiles, nofma=False, n_dump=0, mats=None, huffman=False):
+    """O9.  Returns (sums [S,5], maxs [S,2], y_dump [S,n_dump,m^dims] or None).
+    huffman=True: transform dot products in Huffman order (reading R21)."""
     if mats is None:
         mats = pack_mats(m, r, point_sets)
-    return _sweep(dims, m, r, mats, d_tiles, g_tiles, nofma, False, n_dump)
+    return _sweep(dims, m, r, mats, d_tiles, g_tiles, _mode(nofma, huffman), False, n_dump)
 
 
 def direct32_sweep(dims, m, r, d_tiles, g_tiles, nofma=True):
