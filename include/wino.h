@@ -56,6 +56,12 @@ typedef enum {
 
 /* Sweep flags. */
 #define WINO_SWEEP_NOFMA 1u /* paper arithmetic acc = RN(acc + RN(a*b)) instead of fmaf chains (R13) */
+/* Huffman evaluation order of every transform dot product ("Huffman tree evaluation
+ * order"; reading R21): products RN(coef*x) of the non-zero coefficients
+ * summed along a Huffman tree over |coef| (ties: leaves in index order, then older nodes);
+ * Hadamard product RN(u*v).  Overrides WINO_SWEEP_NOFMA.  Compiled for F(2,3), F(4,3),
+ * F(6,3) in 1D and 2D; other shapes return WINO_E_UNSUPPORTED. */
+#define WINO_SWEEP_HUFFMAN 2u
 
 const char* wino_status_string(int status);
 const char* wino_last_error(void);

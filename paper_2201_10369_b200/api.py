@@ -15,6 +15,7 @@ from ._lib import check, load
 WINO_SUMS = 5
 WINO_MAXS = 2
 WINO_SWEEP_NOFMA = 1
+WINO_SWEEP_HUFFMAN = 2
 WINO_CONV_TF32 = 1
 WINO_MAX_N = 16
 

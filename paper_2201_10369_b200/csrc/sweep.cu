@@ -33,7 +33,9 @@
 //    non-finite e makes Σ|e| non-finite; such a warp re-evaluates the candidate with
 //    per-output checks (the rare degenerate-candidate path).  Σ|y64|, max|y64| do not
 //    depend on the candidate and come from K6 (statistics layout, include/wino.h).
-#include "sweep_kernels.cuh"
+#include <cmath>
+
+#include "sweep_huff.cuh"
 
 namespace wino {
 
@@ -114,6 +116,53 @@ const std::vector<SweepCfg>& cfgs() {
   return v;
 }
 
+const HuffCfg* find_huff(int dims, int m, int r) {
+  static const std::vector<HuffCfg> v = sweep_huff_cfgs();
+  for (const auto& h : v)
+    if (h.dims == dims && h.m == m && h.r == r) return &h;
+  return nullptr;
+}
+
+// Huffman program of one coefficient row (R21; record layout in sweep_huff.cuh):
+// leaves = non-zero coefficients in index order, weight |coef| (fp64); each step joins the
+// two live nodes of smallest (weight, seq) -- leaves have seq = index, node k seq = len + k.
+void huffman_program(const float* row, int len, unsigned char* rec) {
+  double w[2 * WINO_MAX_N];
+  int seq[2 * WINO_MAX_N], slot[2 * WINO_MAX_N];
+  bool live[2 * WINO_MAX_N];
+  int cnt = 0;
+  for (int j = 0; j < len; j++)
+    if (row[j] != 0.0f) {
+      w[cnt] = std::fabs((double)row[j]);
+      seq[cnt] = j;
+      slot[cnt] = j;
+      live[cnt] = true;
+      cnt++;
+    }
+  const int leaves = cnt;
+  const int nops = leaves > 1 ? leaves - 1 : 0;
+  rec[0] = (unsigned char)nops;
+  for (int k = 0; k < nops; k++) {
+    int pick[2];
+    for (int t = 0; t < 2; t++) {
+      int b = -1;
+      for (int i = 0; i < cnt; i++)
+        if (live[i] && (b < 0 || w[i] < w[b] || (w[i] == w[b] && seq[i] < seq[b]))) b = i;
+      live[b] = false;
+      pick[t] = b;
+    }
+    rec[2 + 2 * k] = (unsigned char)slot[pick[0]];
+    rec[3 + 2 * k] = (unsigned char)slot[pick[1]];
+    w[cnt] = w[pick[0]] + w[pick[1]];
+    seq[cnt] = len + k;
+    slot[cnt] = len + k;
+    live[cnt] = true;
+    cnt++;
+  }
+  rec[1] = leaves == 0 ? kHuffNone : (unsigned char)slot[cnt - 1];
+  for (int k = nops; k < len - 1; k++) rec[2 + 2 * k] = rec[3 + 2 * k] = 0;
+}
+
 const SweepCfg* find_cfg(int dims, int m, int r) {
   for (const auto& c : cfgs())
     if (c.dims == dims && c.m == m && c.r == r) return &c;
@@ -164,6 +213,10 @@ WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
     const long long nb = std::max(n_tblk_of(c.dims, lay, n_tiles), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }
+  {  // Huffman kernels: tile pairs, 2 * kSwThreads tiles per block
+    const long long nb = std::max((long long)((n_tiles + 2 * kSwThreads - 1) / (2 * kSwThreads)), 1LL);
+    n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
+  }
   const long long n_ref_blocks = (n_tiles + 255) / 256;
   WsLayout L;
   L.y64 = 0;
@@ -197,14 +250,20 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   const SweepCfg* c = find_cfg(dims, m, r);
   if (!c) return set_error(WINO_E_UNSUPPORTED, "no sweep kernel for dims=%d m=%d r=%d", dims, m, r);
   const bool dump = d_y != nullptr;
+  const bool huff = (flags & WINO_SWEEP_HUFFMAN) != 0;
   const int nofma = (flags & WINO_SWEEP_NOFMA) ? 1 : 0;
+  const HuffCfg* hc = huff ? find_huff(dims, m, r) : nullptr;
+  if (huff && !hc)
+    return set_error(WINO_E_UNSUPPORTED, "no Huffman-order sweep kernel for dims=%d m=%d r=%d", dims, m, r);
   const std::vector<Variant>& variants = c->variants;
   const Layout lay = variants.back().lay[nofma];
   const int n = m + r - 1;
   const int per = per_cand(m, r);
-  int cmax = sweep_max_cands_per_launch(dims, m, r);
+  const int stride = huff ? per + huff_prog_words(m, r) : per;   // floats per candidate in the params
+  int cmax = huff ? std::min(kParamFloats / stride, kMaxCandsLaunch) : sweep_max_cands_per_launch(dims, m, r);
   const int dy = dims == 1 ? m : m * m;
-  const long long n_tblk = n_tiles > 0 ? n_tblk_of(dims, lay, n_tiles) : 0;
+  const long long tpb_h = 2 * kSwThreads;
+  const long long n_tblk = n_tiles <= 0 ? 0 : huff ? (n_tiles + tpb_h - 1) / tpb_h : n_tblk_of(dims, lay, n_tiles);
   const int tpc = tblk_per_cta(std::max(n_tblk, 1LL));
   const int n_tg = (int)((n_tblk + tpc - 1) / tpc);
   const bool work = n_tiles > 0 && n_cand > 0;
@@ -219,8 +278,15 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   double* partial = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.partial);
   double* ref_part = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_part);
   double* ref_tot = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_tot);
-  const size_t smem = smem_bytes(dims, m, r, lay);
-  if (work && smem > 48 * 1024) {
+  const size_t smem = huff ? (size_t)(2 * n - 1) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
+                                 (size_t)kMaxCpc * 4 * kPartial * 8
+                           : smem_bytes(dims, m, r, lay);
+  if (work && huff && smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)hc->k[dump ? 1 : 0],
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  if (work && !huff && smem > 48 * 1024) {
     for (const Variant& v : variants) {
       cudaError_t e = cudaFuncSetAttribute((const void*)v.k[nofma][dump ? 1 : 0],
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -237,7 +303,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   bool refs_done = false;
   MatsParam* P = new MatsParam;
   IdxParam* DI = new IdxParam;
-  std::vector<float> chunk((size_t)cmax * per);
+  std::vector<float> chunk((size_t)cmax * stride);
   std::vector<int> ok(std::max(n_cand, 1), 0);
   double AT[WINO_MAX_N * WINO_MAX_N], G[WINO_MAX_N * WINO_MAX_N], BT[WINO_MAX_N * WINO_MAX_N];
   int i = 0;
@@ -252,7 +318,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
       cand_status[i] = s;
       if (s == WINO_OK) {
         ok[i] = 1;
-        float* dst = chunk.data() + (size_t)nc * per;
+        float* dst = chunk.data() + (size_t)nc * stride;
         // non-zero positions; a matrix with more than 64 entries has no specialised
         // variant, so its mask saturates (all bits set = "nothing may be skipped")
         for (int t = 0; t < m * n; t++) {
@@ -267,13 +333,22 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
           dst[m * n + n * r + t] = (float)BT[t];
           if (dst[m * n + n * r + t] != 0.0f) nzB |= t < 64 ? 1ull << t : ~0ull;
         }
+        if (huff) {   // programs after the matrices: G rows, Bᵀ rows, Aᵀ rows
+          unsigned char* pr = reinterpret_cast<unsigned char*>(dst + per);
+          std::fill(pr, pr + 4 * huff_prog_words(m, r), (unsigned char)0);
+          for (int q = 0; q < n; q++) huffman_program(dst + m * n + q * r, r, pr + q * huff_rec_bytes(r));
+          pr += n * huff_rec_bytes(r);
+          for (int q = 0; q < n; q++) huffman_program(dst + m * n + n * r + q * n, n, pr + q * huff_rec_bytes(n));
+          pr += n * huff_rec_bytes(n);
+          for (int q = 0; q < m; q++) huffman_program(dst + q * n, n, pr + q * huff_rec_bytes(n));
+        }
         DI->idx[nc] = i;
         nc++;
       }
       i++;
     }
     if (nc == 0 || n_tiles <= 0) continue;
-    std::copy(chunk.data(), chunk.data() + (size_t)nc * per, P->v);
+    std::copy(chunk.data(), chunk.data() + (size_t)nc * stride, P->v);
     if (!dump && !refs_done) {
       const int tpb = 256;
       const unsigned nb = (unsigned)((n_tiles + tpb - 1) / tpb);
@@ -292,7 +367,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
         var = &v;
         break;
       }
-    SweepKernel kern = var->k[nofma][dump ? 1 : 0];
+    SweepKernel kern = huff ? hc->k[dump ? 1 : 0] : var->k[nofma][dump ? 1 : 0];
     // Work item = (up to cpc candidates, one tile group).  Persistent grid of one wave of
     // resident CTAs walking the items round-robin; cpc is chosen (<= kMaxCpc, larger is
     // better for amortising the tile loads) so the items fill whole rounds of the wave.
@@ -326,7 +401,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     args.n_tgroups = n_tg;
     args.n_cgroups = groups;
     dim3 grid((unsigned)std::min<long long>(n_items, slots));
-    timed_launch(dims == 1 ? "sweep1d" : "sweep2d", stream,
+    timed_launch(huff ? "sweep_huffman" : dims == 1 ? "sweep1d" : "sweep2d", stream,
                  [&] { kern<<<grid, kSwThreads, smem, stream>>>(args, *P, *DI); });
     launches++;
     cudaError_t e = cudaGetLastError();

@@ -1,0 +1,240 @@
+// NEXT row N2: the error sweep with Huffman-ordered transforms (WINO_SWEEP_HUFFMAN).
+// PAPER.md P:465 ("Huffman tree evaluation order ... We also use the same evaluation order
+// and present results based on it"); reading R21: every dot product of a
+// transform row with data is the sum of the products RN(coef_j * x_j) of the non-zero
+// coefficients along a Huffman tree over |coef_j| (ties: leaves in index order, then older
+// nodes); the Hadamard product is RN(u * v).
+//
+// The tree depends on the candidate's coefficients, so it cannot be unrolled at compile
+// time.  The host builds, per candidate and matrix row, a small program (huffman_program in
+// sweep.cu): `nops` additions (a, b) over slots 0..len-1 (the products, by coefficient
+// index) and len.. (the internal nodes in creation order), plus the result slot (255: no
+// term, +0).  The programs ride in the kernel parameter space after the candidate's
+// matrices; the kernel forms the products with FMUL2 (two tiles per thread), keeps them in
+// a per-thread column of shared memory ([slot][thread], conflict-free) and executes the
+// additions with FADD2 in program order.  Scoring as in the fp64 paths (Stat, careful).
+// Kernel and host agree on the record layout below; outputs are bit-identical to the
+// oracle's Huffman mode (tests/test_gpu_huffman.py).
+#pragma once
+#include "sweep_kernels.cuh"
+
+namespace wino {
+
+// per-row program record: [nops][result][a0 b0][a1 b1]...  (2 + 2 * (len - 1) bytes)
+__host__ __device__ constexpr int huff_rec_bytes(int len) { return 2 + 2 * (len - 1); }
+// per-candidate program bytes: n rows of G (len r), n rows of Bᵀ (len n), m rows of Aᵀ (len n)
+__host__ __device__ constexpr int huff_prog_bytes(int m, int r) {
+  return (m + r - 1) * huff_rec_bytes(r) + (m + r - 1) * huff_rec_bytes(m + r - 1) + m * huff_rec_bytes(m + r - 1);
+}
+__host__ __device__ constexpr int huff_prog_words(int m, int r) { return (huff_prog_bytes(m, r) + 3) / 4; }
+constexpr unsigned char kHuffNone = 255;
+
+__device__ __forceinline__ u64 hmul2(u64 a, float c) {
+  u64 d, cc;
+  asm("mov.b64 %0, {%1,%1};" : "=l"(cc) : "f"(c));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(cc));
+  return d;
+}
+__device__ __forceinline__ u64 hmulv2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 hadd2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Σ_j coef[j * cs] * x[j] in the row's Huffman order.  `slot` = this thread's column
+// (stride kSwThreads u64); `rec` = the row's program record (parameter space).
+template <int LEN>
+__device__ __forceinline__ u64 huff_dot(const float* coef, int cs, const u64 (&x)[LEN], const unsigned char* rec,
+                                        u64* slot) {
+#pragma unroll
+  for (int j = 0; j < LEN; j++) slot[j * kSwThreads] = hmul2(x[j], coef[j * cs]);
+  const int nops = rec[0];
+#pragma unroll
+  for (int k = 0; k < LEN - 1; k++) {
+    if (k < nops) {
+      const int a = rec[2 + 2 * k], b = rec[3 + 2 * k];
+      slot[(LEN + k) * kSwThreads] = hadd2(slot[a * kSwThreads], slot[b * kSwThreads]);
+    }
+  }
+  const int res = rec[1];
+  return res == kHuffNone ? 0ull : slot[res * kSwThreads];
+}
+
+// smem: slots [2N-1][kSwThreads] u64, y64 [MM][2][kSwThreads] double, sacc
+template <int DIMS, int M, int R, bool DUMP>
+__global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+                                                                const __grid_constant__ IdxParam DI) {
+  constexpr int N = M + R - 1;
+  constexpr int DN = DIMS == 1 ? N : N * N, DG = DIMS == 1 ? R : R * R, DY = DIMS == 1 ? M : M * M;
+  constexpr int PER = M * N + N * R + N * N;
+  constexpr int STRIDE = PER + huff_prog_words(M, R);
+  constexpr int TPB = kSwThreads * 2;
+  constexpr int RG = huff_rec_bytes(R), RB = huff_rec_bytes(N);
+  extern __shared__ __align__(16) unsigned char smem[];
+  u64* slots = reinterpret_cast<u64*>(smem);                        // [2N-1][kSwThreads]
+  double* sy = reinterpret_cast<double*>(slots + (2 * N - 1) * kSwThreads);   // [DY][2][kSwThreads]
+  double* sacc = sy + DY * 2 * kSwThreads;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  u64* slot = slots + tid;
+
+  const int n_items = a.n_cgroups * a.n_tgroups;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+    const int c_begin = cg * a.cands_per_cta;
+    const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+    __syncthreads();
+    if (!DUMP)
+      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    const int tb_begin = tg * a.tblk_per_cta;
+    const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+    for (int tb = tb_begin; tb < tb_end; tb++) {
+      const long long tile0 = (long long)tb * TPB;
+      bool ok[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) ok[h] = tile0 + tid + h * kSwThreads < a.n_tiles;
+      u64 d[DN], g[DG];
+#pragma unroll
+      for (int e = 0; e < DN; e++) {
+        float v[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) v[h] = ok[h] ? __ldg(a.d + (tile0 + tid + h * kSwThreads) * DN + e) : 0.0f;
+        d[e] = Lane<true, true>::pack(v[0], v[1]);
+      }
+#pragma unroll
+      for (int e = 0; e < DG; e++) {
+        float v[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) v[h] = ok[h] ? __ldg(a.g + (tile0 + tid + h * kSwThreads) * DG + e) : 0.0f;
+        g[e] = Lane<true, true>::pack(v[0], v[1]);
+      }
+      if (!DUMP)
+#pragma unroll
+        for (int o = 0; o < DY; o++)
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+            sy[(o * 2 + h) * kSwThreads + tid] = ok[h] ? __ldg(a.y64 + (tile0 + tid + h * kSwThreads) * DY + o) : 0.0;
+
+      for (int s = c_begin; s < c_end; s++) {
+        const float* cm = P.v + s * STRIDE;
+        const float* AT = cm;
+        const float* G = cm + M * N;
+        const float* BT = cm + M * N + N * R;
+        const unsigned char* pg = reinterpret_cast<const unsigned char*>(cm + PER);   // G rows
+        const unsigned char* pb = pg + N * RG;                                        // Bᵀ rows
+        const unsigned char* pa = pb + N * RB;                                        // Aᵀ rows
+        u64 y[DY];
+        if constexpr (DIMS == 1) {
+          u64 mw[N];
+#pragma unroll
+          for (int i = 0; i < N; i++) {
+            const u64 u = huff_dot<R>(G + i * R, 1, g, pg + i * RG, slot);
+            const u64 v = huff_dot<N>(BT + i * N, 1, d, pb + i * RB, slot);
+            mw[i] = hmulv2(u, v);
+          }
+#pragma unroll
+          for (int p = 0; p < M; p++) y[p] = huff_dot<N>(AT + p * N, 1, mw, pa + p * RB, slot);
+        } else {
+          // U = G g Gᵀ: T1[i][q] = dot(G row i, g[.][q]); U[i][l] = dot(G row l, T1[i][.])
+          u64 U[N][N];
+#pragma unroll
+          for (int i = 0; i < N; i++) {
+            u64 t1[R];
+#pragma unroll
+            for (int q = 0; q < R; q++) {
+              u64 col[R];
+#pragma unroll
+              for (int j = 0; j < R; j++) col[j] = g[j * R + q];
+              t1[q] = huff_dot<R>(G + i * R, 1, col, pg + i * RG, slot);
+            }
+#pragma unroll
+            for (int l = 0; l < N; l++) U[i][l] = huff_dot<R>(G + l * R, 1, t1, pg + l * RG, slot);
+          }
+          // V = Bᵀ d B row by row, Mw = U ⊙ V (kept in U)
+#pragma unroll
+          for (int i = 0; i < N; i++) {
+            u64 t2[N];
+#pragma unroll
+            for (int q = 0; q < N; q++) {
+              u64 col[N];
+#pragma unroll
+              for (int j = 0; j < N; j++) col[j] = d[j * N + q];
+              t2[q] = huff_dot<N>(BT + i * N, 1, col, pb + i * RB, slot);
+            }
+#pragma unroll
+            for (int l = 0; l < N; l++) U[i][l] = hmulv2(U[i][l], huff_dot<N>(BT + l * N, 1, t2, pb + l * RB, slot));
+          }
+          // Y = Aᵀ Mw A: T3[p][l] = dot(Aᵀ row p, Mw[.][l]); Y[p][s] = dot(Aᵀ row s, T3[p][.])
+#pragma unroll
+          for (int p = 0; p < M; p++) {
+            u64 t3[N];
+#pragma unroll
+            for (int l = 0; l < N; l++) {
+              u64 col[N];
+#pragma unroll
+              for (int i = 0; i < N; i++) col[i] = U[i][l];
+              t3[l] = huff_dot<N>(AT + p * N, 1, col, pa + p * RB, slot);
+            }
+#pragma unroll
+            for (int q = 0; q < M; q++) y[p * M + q] = huff_dot<N>(AT + q * N, 1, t3, pa + q * RB, slot);
+          }
+        }
+        if (DUMP) {
+          float* yd = a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * DY;
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+            if (ok[h])
+#pragma unroll
+              for (int o = 0; o < DY; o++) yd[(tid + h * kSwThreads) * DY + o] = Lane<true, true>::get(y[o], h);
+        } else {
+          Stat st;
+#pragma unroll
+          for (int o = 0; o < DY; o++) {
+            if (ok[0]) st.add_careful<0>(Lane<true, true>::get(y[o], 0), sy[(o * 2) * kSwThreads + tid]);
+            if (ok[1]) st.add_careful<1>(Lane<true, true>::get(y[o], 1), sy[(o * 2 + 1) * kSwThreads + tid]);
+          }
+          st.warp_reduce();
+          if (lane == 0) {
+            double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
+            acc[0] += st.s0[0];
+            acc[1] += st.s1[0];
+            acc[2] = st.m0[0] > acc[2] ? st.m0[0] : acc[2];
+            acc[3] += (double)st.nonfin;
+          }
+        }
+      }
+    }
+    if (!DUMP) {
+      __syncthreads();
+      for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
+        double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < 4; w++) {
+          const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
+          v[0] += acc[0];
+          v[1] += acc[1];
+          v[2] = acc[2] > v[2] ? acc[2] : v[2];
+          v[3] += acc[3];
+        }
+        double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
+        for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+      }
+    }
+  }
+}
+
+template <int DIMS, int M, int R>
+HuffCfg make_huff_cfg() {
+  HuffCfg h;
+  h.dims = DIMS;
+  h.m = M;
+  h.r = R;
+  h.k[0] = (SweepKernel)sweep_huff_kernel<DIMS, M, R, false>;
+  h.k[1] = (SweepKernel)sweep_huff_kernel<DIMS, M, R, true>;
+  return h;
+}
+
+}  // namespace wino

@@ -954,11 +954,18 @@ inline constexpr uint64_t kF43A = 0x124920ull, kF43G = 0x18180ull, kF43B = 0x561
 inline constexpr uint64_t kF23A = 0x28ull, kF23G = 0x630ull, kF23B = 0x59a9ull;
 
 
+// Huffman-order sweep kernels (sweep_huff.cuh), [dump]
+struct HuffCfg {
+  int dims, m, r;
+  SweepKernel k[2];
+};
+
 // per-translation-unit registries (sweep_inst_*.cu)
 std::vector<SweepCfg> sweep_cfgs_1d();
 std::vector<SweepCfg> sweep_cfgs_1d_large();
 std::vector<SweepCfg> sweep_cfgs_2d_f43();
 std::vector<SweepCfg> sweep_cfgs_2d_small();
 std::vector<SweepCfg> sweep_cfgs_2d_large();
+std::vector<HuffCfg> sweep_huff_cfgs();
 
 }  // namespace wino

@@ -1,0 +1,100 @@
+"""NEXT row N2: the Huffman-order sweep (WINO_SWEEP_HUFFMAN) against the oracle's Huffman
+mode (reading R21): per-element fp32 outputs bit-identical, statistics within the
+sweep tolerances, the paper's Huffman-ordered F(4,3) rows reproduced on the GPU path, and
+the unsupported-shape error."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import points as OP, ref
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+HUFF = 2
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _outputs(dims, m, r, sets, d, g):
+    import torch
+    from paper_2201_10369_b200 import api
+    y = torch.full((len(sets), d.shape[0], m ** dims), float("nan"), dtype=torch.float32, device="cuda")
+    st = api.wino_sweep_outputs(dims, m, r, np.array(sets), _dev(d), _dev(g), y, flags=HUFF)
+    torch.cuda.synchronize()
+    return st, y.cpu().numpy()
+
+
+def _stats(dims, m, r, sets, d, g):
+    import torch
+    from paper_2201_10369_b200 import api
+    S, T = len(sets), d.shape[0]
+    sums = torch.zeros((S, 5), dtype=torch.float64, device="cuda")
+    maxs = torch.zeros((S, 2), dtype=torch.float64, device="cuda")
+    ws = torch.empty(api.wino_error_sweep_workspace_bytes(dims, m, r, S, T), dtype=torch.uint8, device="cuda")
+    st = api.wino_error_sweep(dims, m, r, np.array(sets), _dev(d), _dev(g), sums, maxs, ws, flags=HUFF)
+    torch.cuda.synchronize()
+    return st, sums.cpu().numpy(), maxs.cpu().numpy()
+
+
+SETS = {
+    2: [OP.f23_c(1.0), OP.f23_c(1.7), [-2.0, 0.5, 1.0, INF]],
+    4: [OP.f43_c(1.622), OP.f43_c(1.829), OP.f43_c(0.3), [-1.0, 0.0, 0.5, 1.0, 2.0, INF],
+        [-3.0, -1.0, 0.0, 0.5, 1.0, INF]],
+    6: [OP.n8_cd(2.0, 1.003), OP.P8],
+}
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+@pytest.mark.parametrize("m", [2, 4, 6])
+def test_huffman_outputs_bitexact(dims, m):
+    sets = [sorted(p for p in s if p != INF) + [INF] for s in SETS[m]]
+    d, g = synth.random_tiles(1031, dims, m + 2, 3, "normal", seed=31)
+    st, y = _outputs(dims, m, 3, sets, d, g)
+    assert np.all(st == 0)
+    _, _, y_ref = ref.sweep(dims, m, 3, sets, d, g, huffman=True, n_dump=d.shape[0])
+    assert np.array_equal(y, y_ref)
+    # and it is a different arithmetic from the sequential NOFMA order
+    _, _, y_seq = ref.sweep(dims, m, 3, sets, d, g, nofma=True, n_dump=d.shape[0])
+    assert not np.array_equal(y, y_seq)
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+def test_huffman_stats(dims):
+    grid = synth.c_grid()
+    cs = [float(grid[i]) for i in range(0, 4096, 97)]
+    sets = [OP.f43_c(c) for c in cs]
+    d, g = synth.random_tiles(20_011, dims, 6, 3, "uniform", seed=12)
+    st, s, mx = _stats(dims, 4, 3, sets, d, g)
+    assert np.all(st == 0)
+    s_ref, m_ref, _ = ref.sweep(dims, 4, 3, sets, d, g, huffman=True)
+    assert np.array_equal(s[:, 3], s_ref[:, 3]) and np.array_equal(s[:, 4], s_ref[:, 4])
+    assert np.array_equal(mx, m_ref)                       # fp64 scoring: max exact
+    assert np.all(np.abs(s[:, 0] / s_ref[:, 0] - 1) < 1e-12)
+    assert np.all(np.abs(s[:, 1] / s_ref[:, 1] - 1) < 1e-12)
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+def test_huffman_paper_rows_on_gpu(dims):
+    """T7/T8 n=6 through the C ABI: within [-3 %, +5 %] of the paper."""
+    import json, os
+    paper = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_error_values.json")))
+    key = "1d" if dims == 1 else "2d"
+    prop, prior = paper[f"f43_proposed_{key}"], paper[f"f43_prior_{key}"]
+    base = OP.F43_PRIOR_1D if dims == 1 else OP.F43_PRIOR_2D
+    d, g = synth.random_tiles(100_000, dims, 6, 3, "uniform", seed=0)
+    st, s, _ = _stats(dims, 4, 3, [OP.f43_c(prop["c"]), base], d, g)
+    e = s[:, 0] / s[:, 3]
+    assert 0.97 <= e[0] / prop["value"] <= 1.05 and 0.97 <= e[1] / prior["value"] <= 1.05
+
+
+def test_huffman_unsupported_shape():
+    from paper_2201_10369_b200 import _lib
+    d, g = synth.random_tiles(100, 2, 8, 5, "uniform", seed=1)
+    with pytest.raises(_lib.WinoError) as ei:
+        _stats(2, 4, 5, [OP.n8_c1c2(1.5, 3.1)], d, g)
+    assert ei.value.status == 8
