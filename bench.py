@@ -388,7 +388,7 @@ def main():
         except Exception:
             traffic = None
     roofline = {
-        "kernel": "sweep2d_kernel<4,3> (K7, 2D F(4x4,3x3))", "bound": "alu", "achieved": achieved,
+        "kernel": "sweep2d_reg_kernel<4,3> (K7, 2D F(4x4,3x3), tile pairs in registers)", "bound": "alu", "achieved": achieved,
         "peak": fp32_peak, "unit": "TFLOP/s", "frac": (achieved / fp32_peak) if achieved else None,
         "traffic": traffic,
         "peak_source": f"FP32 FFMA: {nsm} SMs x 128 lanes x 2 FLOP x {fmax:.0f} MHz (sm_max_mhz, {peak_src}); "
@@ -450,6 +450,33 @@ def main():
         layer["roofline_frac"] = t_roof / (t_layer * 1e-3)
         layer["roofline_bound"] = "fp32 FFMA (t_roof = max(F_alg/P_fp32, B_alg/BW_hbm))"
 
+    # NEXT row N2: the Huffman-order variant of the configs[1] 2D uniform sweep, timed once
+    variants = None
+    if rank == 0 and world == 1 and not args.no_layer:
+        variants = {}
+        from paper_2201_10369_b200 import api
+        sp = next(r for r in rsw if r.spec.dims == 2)
+        sets, dd, gg = sp.sets, sp.d_tiles, sp.g_tiles           # the rank's shard = the whole job at N=1
+        S, T = len(sets), sp.spec.n_tiles
+        hws = torch.empty(api.wino_error_sweep_workspace_bytes(2, 4, 3, S, T), dtype=torch.uint8, device=dev)
+        hs = torch.zeros((S, 5), dtype=torch.float64, device=dev)
+        hm = torch.zeros((S, 2), dtype=torch.float64, device=dev)
+        api.wino_error_sweep(2, 4, 3, sets, dd, gg, hs, hm, hws, flags=api.WINO_SWEEP_HUFFMAN)   # warm-up
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.wino_error_sweep(2, 4, 3, sets, dd, gg, hs, hm, hws, flags=api.WINO_SWEEP_HUFFMAN)
+        b.record(stream)
+        b.synchronize()
+        hms = a.elapsed_time(b)
+        mae = curve(hs.cpu().numpy() / 2)
+        i, best = argmin_c(sp.spec.params, mae)
+        variants["huffman_2d"] = {
+            "workload": f"configs[1] 2D {sp.spec.dist} sweep ({S} c x {T} tiles), WINO_SWEEP_HUFFMAN (reading R21)",
+            "ms": hms, "value": S * T / (hms * 1e-3), "unit": "tile-evals/s",
+            "argmin_c": float(sp.spec.params[i]) if i is not None else None, "min_mae": best}
+        del hws
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         evals_c, dt_c, thr, desc = oracle_sample_run(specs, args.ref_every)
@@ -479,6 +506,7 @@ def main():
             "step_ms": step_ms,
             "results": results,
             "layer": layer,
+            "variants": variants,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
