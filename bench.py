@@ -227,25 +227,29 @@ def bench_layer(torch, dev, flush, steps=10):
         b.record(stream)
         b.synchronize()
         sc.append(a.elapsed_time(b))
-    # NEXT row N3: the tcgen05 kind::tf32 contraction variant (not the parity path)
-    tf = []
-    api.wino_timing_reset()
-    for _ in range(steps):
-        flush()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, flags=api.WINO_CONV_TF32)
-        b.record(stream)
-        b.synchronize()
-        tf.append(a.elapsed_time(b))
-    kern_tf = {f: api.wino_timing_read(f)[0] / steps
-               for f in ["layer_filter", "layer_input", "layer_gemm_tf32", "layer_output"]}
-    sums_tf = torch.zeros(5, dtype=torch.float64, device=dev)
-    maxs_tf = torch.zeros(2, dtype=torch.float64, device=dev)
-    api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sums_tf, maxs_tf, flags=api.WINO_CONV_TF32)
-    torch.cuda.synchronize()
+    # NEXT row N3: the tcgen05 kind::tf32 contraction variants (not the parity path)
+    def run_variant(flag, gemm_family):
+        tv = []
+        api.wino_timing_reset()
+        for _ in range(steps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, flags=flag)
+            b.record(stream)
+            b.synchronize()
+            tv.append(a.elapsed_time(b))
+        kv = {f: api.wino_timing_read(f)[0] / steps
+              for f in ["layer_filter", "layer_input", gemm_family, "layer_output"]}
+        sv = torch.zeros(5, dtype=torch.float64, device=dev)
+        mv = torch.zeros(2, dtype=torch.float64, device=dev)
+        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sv, mv, flags=flag)
+        torch.cuda.synchronize()
+        return tv, kv, sv.cpu().numpy()
+
+    tf, kern_tf, s_tf = run_variant(api.WINO_CONV_TF32, "layer_gemm_tf32")
+    tf3, kern_tf3, s_tf3 = run_variant(api.WINO_CONV_3XTF32, "layer_gemm_3xtf32")
     api.wino_timing_enable(False)
-    s_tf = sums_tf.cpu().numpy()
     s = sums.cpu().numpy() / 2
     t = statistics.median(ts)
     direct_flop = 2.0 * N * K * C * Ho * Wo * r * r
@@ -275,6 +279,18 @@ def bench_layer(torch, dev, flush, steps=10):
         "note": "WINO_CONV_TF32: tcgen05.mma kind::tf32 (TMA-fed, TMEM accumulators); operands rounded to "
                 "TF32, so NOT the fp32 parity path -- reported separately",
     }
+    t_tf3 = statistics.median(tf3)
+    g3 = kern_tf3["layer_gemm_3xtf32"]
+    gemm_bytes3 = 4.0 * n * n * (2 * Cp * Kp + 2 * Cp * Tp + Kp * Tp)   # hi + lo planes of U and V
+    tf32x3 = {
+        "ms": t_tf3, "effective_tflops": direct_flop / (t_tf3 * 1e-3) / 1e12, "kernel_ms": kern_tf3,
+        "gemm_tflops": 2.0 * gemm_mac / (g3 * 1e-3) / 1e12 if g3 else None,
+        "gemm_roofline": {"bound": "hbm", "achieved_gbs": gemm_bytes3 / (g3 * 1e-3) / 1e9 if g3 else None,
+                          "peak_gbs": peaks["hbm_gbs"], "peak_source": psrc,
+                          "frac": gemm_bytes3 / (g3 * 1e-3) / 1e9 / peaks["hbm_gbs"] if g3 else None},
+        "scored_mae": float(s_tf3[0] / s_tf3[3]) if s_tf3[3] else None,
+        "note": "WINO_CONV_3XTF32: hi/lo split, 3 tcgen05 MMAs per step; ~fp32 accuracy, not bitwise parity",
+    }
     return {
         "workload": "configs[2] F(6x6,3x3) N=32 C=K=256 56x56 pad 1, points {0,±2,±1/2,-1/1.003,1.003,inf}",
         "ms": t, "ms_min": min(ts), "effective_tflops": direct_flop / (t * 1e-3) / 1e12,
@@ -282,6 +298,7 @@ def bench_layer(torch, dev, flush, steps=10):
         "scored_ms": statistics.median(sc), "scored_mae": float(s[0] / s[3]) if s[3] else None,
         "l2": "flushed (512 MB write) before every run",
         "tf32_variant": tf32,
+        "tf32x3_variant": tf32x3,
     }, f_alg, b_alg, t
 
 

@@ -112,6 +112,11 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y,
  *   each operand, so this variant does NOT have the parity semantics above; its error is
  *   what the scored statistics measure.  Same arguments and workspace as (2). */
 #define WINO_CONV_TF32 1u
+/*   WINO_CONV_3XTF32: split-precision contraction on the same tensor cores: each operand is
+ *   x = hi + lo (hi = tf32(x), lo = tf32(x - hi)) and M += lo*hi + hi*lo + hi*hi with fp32
+ *   accumulation, recovering ~fp32 accuracy (not bit-identical to the parity path).  Takes
+ *   precedence over WINO_CONV_TF32. */
+#define WINO_CONV_3XTF32 2u
 int wino_conv2d_fp32_ex(const float* x, const float* w, float* y,
                         int N, int C, int H, int W, int K, int r, int pad, int m,
                         const double* points, void* workspace, size_t workspace_bytes,
@@ -154,7 +159,7 @@ int wino_last_launch_count(void);
 /* Kernel timing hook (profiling / bench.py roofline).  While enabled, every launch is
  * bracketed by two cudaEvents recorded on its own stream and filed under its kernel
  * family: "sweep1d", "sweep2d", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
- * "layer_filter", "layer_input", "layer_gemm", "layer_gemm_tf32", "layer_output", "layer_score",
+ * "layer_filter", "layer_input", "layer_gemm", "layer_gemm_tf32", "layer_gemm_3xtf32", "layer_output", "layer_score",
  * "layer_score_finalize", "relu_pool".  wino_timing_read() synchronises on the recorded events and
  * returns the summed milliseconds and launch count of one family since the last reset.
  * Returns the previous enable state / a wino_status. */

@@ -17,6 +17,7 @@ WINO_MAXS = 2
 WINO_SWEEP_NOFMA = 1
 WINO_SWEEP_HUFFMAN = 2
 WINO_CONV_TF32 = 1
+WINO_CONV_3XTF32 = 2
 WINO_MAX_N = 16
 
 _d = ctypes.POINTER(ctypes.c_double)

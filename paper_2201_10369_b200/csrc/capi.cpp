@@ -159,7 +159,7 @@ int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, 
   if (!x || !w || !y || !points) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || r < 1 || m < 1 || pad < 0)
     return set_error(WINO_E_INVALID_ARG, "non-positive size or negative pad");
-  if (flags & ~WINO_CONV_TF32) return set_error(WINO_E_INVALID_ARG, "unknown flags");
+  if (flags & ~(WINO_CONV_TF32 | WINO_CONV_3XTF32)) return set_error(WINO_E_INVALID_ARG, "unknown flags");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
   if (H + 2 * pad < r || W + 2 * pad < r) return set_error(WINO_E_BAD_SHAPE, "empty output");

@@ -39,7 +39,8 @@ struct Geo {
   long long T;     // tiles = N * th * tw
   int Cp, Kp;
   long long Tp;
-  int tf32;        // 1: U / V are rounded to TF32 (nearest, ties away) for the tcgen05 variant
+  int tf32;        // 1: U / V rounded to TF32 (nearest, ties away) for the tcgen05 variant;
+                   // 2: 3xTF32 -- hi = tf32(x) in plane p, lo = tf32(x - hi) in plane NN + p
 };
 
 // round-to-nearest fp32 -> TF32 (10 explicit mantissa bits); the tensor core would otherwise
@@ -50,7 +51,7 @@ __device__ __forceinline__ float round_tf32(float v) {
   return __uint_as_float(r);
 }
 
-Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, bool tf32 = false) {
+Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, int tf32 = 0) {
   Geo g;
   g.N = N; g.C = C; g.H = H; g.W = W; g.K = K; g.r = r; g.pad = pad; g.m = m;
   g.Ho = H + 2 * pad - r + 1;
@@ -63,7 +64,7 @@ Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, bool tf32
   g.Cp = (C + ca - 1) / ca * ca;
   g.Kp = (K + 127) / 128 * 128;
   g.Tp = (g.T + ta - 1) / ta * ta;
-  g.tf32 = tf32 ? 1 : 0;
+  g.tf32 = tf32;
   return g;
 }
 
@@ -79,7 +80,7 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
   const long long plane = (long long)Cp * Kp;
   if (k >= K || c >= C) {
 #pragma unroll
-    for (int p = 0; p < N * N; p++) U[p * plane + idx] = 0.0f;
+    for (int p = 0; p < (tf32 == 2 ? 2 : 1) * N * N; p++) U[p * plane + idx] = 0.0f;
     return;
   }
   float g[R * R];
@@ -103,7 +104,13 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
       float acc = 0.0f;
 #pragma unroll
       for (int q = 0; q < R; q++) acc = __fmaf_rn(t1[i][q], mt.G[l * R + q], acc);
-      U[(i * N + l) * plane + idx] = tf32 ? round_tf32(acc) : acc;
+      if (tf32 == 2) {
+        const float hi = round_tf32(acc);
+        U[(i * N + l) * plane + idx] = hi;
+        U[(N * N + i * N + l) * plane + idx] = round_tf32(acc - hi);
+      } else {
+        U[(i * N + l) * plane + idx] = tf32 ? round_tf32(acc) : acc;
+      }
     }
 }
 
@@ -120,7 +127,7 @@ __global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V,
   const long long plane = (long long)geo.Cp * geo.Tp;
   if (t >= geo.T || c >= geo.C) {
 #pragma unroll
-    for (int p = 0; p < N * N; p++) V[p * plane + idx] = 0.0f;
+    for (int p = 0; p < (geo.tf32 == 2 ? 2 : 1) * N * N; p++) V[p * plane + idx] = 0.0f;
     return;
   }
   const int per_img = geo.th * geo.tw;
@@ -156,7 +163,13 @@ __global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V,
       float acc = 0.0f;
 #pragma unroll
       for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
-      V[(i * N + l) * plane + idx] = geo.tf32 ? round_tf32(acc) : acc;
+      if (geo.tf32 == 2) {
+        const float hi = round_tf32(acc);
+        V[(i * N + l) * plane + idx] = hi;
+        V[(N * N + i * N + l) * plane + idx] = round_tf32(acc - hi);
+      } else {
+        V[(i * N + l) * plane + idx] = geo.tf32 ? round_tf32(acc) : acc;
+      }
     }
 }
 
@@ -497,8 +510,9 @@ WsLayout ws_layout(const Geo& g) {
   const int n = g.m + g.r - 1, nn = n * n;
   WsLayout L;
   L.u_off = 0;
-  L.v_off = L.u_off + align_up((size_t)nn * g.Cp * g.Kp * sizeof(float), 256);
-  L.m_off = L.v_off + align_up((size_t)nn * g.Cp * g.Tp * sizeof(float), 256);
+  const size_t planes = g.tf32 == 2 ? 2 : 1;   // 3xTF32: hi and lo planes of U and V
+  L.v_off = L.u_off + align_up(planes * nn * g.Cp * g.Kp * sizeof(float), 256);
+  L.m_off = L.v_off + align_up(planes * nn * g.Cp * g.Tp * sizeof(float), 256);
   L.p_off = L.m_off + align_up((size_t)nn * g.Kp * g.Tp * sizeof(float), 256);
   const dim3 sg = score_grid(g);
   L.total = L.p_off + align_up((size_t)sg.x * sg.y * sg.z * 8 * sizeof(double), 256);
@@ -539,8 +553,8 @@ int layer_supported(int m, int r) { return find_layer(m, r) != nullptr; }
 
 size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m) {
   // large enough for the FFMA path and the tcgen05 variant's alignments
-  return std::max(ws_layout(make_geo(N, C, H, W, K, r, pad, m, false)).total,
-                  ws_layout(make_geo(N, C, H, W, K, r, pad, m, true)).total);
+  return std::max(ws_layout(make_geo(N, C, H, W, K, r, pad, m, 0)).total,
+                  ws_layout(make_geo(N, C, H, W, K, r, pad, m, 2)).total);
 }
 
 int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
@@ -548,7 +562,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
                  double* d_sums, double* d_maxs, unsigned flags, cudaStream_t stream) {
   const LayerCfg* cfg = find_layer(m, r);
   if (!cfg) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
-  const bool tf32 = (flags & WINO_CONV_TF32) != 0;
+  const int tf32 = (flags & WINO_CONV_3XTF32) ? 2 : (flags & WINO_CONV_TF32) ? 1 : 0;
   const Geo g = make_geo(N, C, H, W, K, r, pad, m, tf32);
   const WsLayout L = ws_layout(g);
   if (!workspace || ws_bytes < L.total)
@@ -583,10 +597,12 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   }
   {
     if (tf32) {
-      static bool tattr = false;
-      if (!tattr) {
-        cudaFuncSetAttribute((const void*)gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmem);
-        tattr = true;
+      static bool tattr[2] = {false, false};
+      const auto kern = tf32 == 2 ? gemm_tf32_kernel<3> : gemm_tf32_kernel<1>;
+      const int smem = tf32 == 2 ? tc::Cfg<3>::kSmem : tc::Cfg<1>::kSmem;
+      if (!tattr[tf32 - 1]) {
+        cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        tattr[tf32 - 1] = true;
       }
       static int n_sm = 0;
       if (!n_sm) {
@@ -596,14 +612,21 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
       }
       const long long tiles = (long long)(n * n) * (g.Kp / tc::kM) * (g.Tp / tc::kN);
       const unsigned grid = (unsigned)std::min<long long>(tiles, n_sm);
-      CUtensorMap tmU, tmV, tmM;
+      CUtensorMap tmU, tmV, tmUl, tmVl, tmM;
       const unsigned long long pc = (unsigned long long)(n * n) * g.Cp, pk = (unsigned long long)(n * n) * g.Kp;
-      if (!tc::encode_map_2d(&tmU, U, (unsigned long long)g.Kp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
-          !tc::encode_map_2d(&tmV, V, (unsigned long long)g.Tp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
-          !tc::encode_map_2d(&tmM, Mw, (unsigned long long)g.Tp, pk, CU_TENSOR_MAP_SWIZZLE_128B))
-        return set_error(WINO_E_CUDA, "cuTensorMapEncodeTiled failed for the tf32 contraction");
-      timed_launch("layer_gemm_tf32", stream, [&] {
-        gemm_tf32_kernel<<<grid, tc::kThreads, tc::kSmem, stream>>>(tmU, tmV, tmM, g.Cp, g.Kp, g.Tp, n * n);
+      const float* Ul = U + (size_t)(n * n) * g.Cp * g.Kp;   // lo planes (3xTF32)
+      const float* Vl = V + (size_t)(n * n) * g.Cp * g.Tp;
+      bool enc = tc::encode_map_2d(&tmU, U, (unsigned long long)g.Kp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+                 tc::encode_map_2d(&tmV, V, (unsigned long long)g.Tp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+                 tc::encode_map_2d(&tmM, Mw, (unsigned long long)g.Tp, pk, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (tf32 == 2)
+        enc = enc && tc::encode_map_2d(&tmUl, Ul, (unsigned long long)g.Kp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+              tc::encode_map_2d(&tmVl, Vl, (unsigned long long)g.Tp, pc, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      else
+        tmUl = tmU, tmVl = tmV;
+      if (!enc) return set_error(WINO_E_CUDA, "cuTensorMapEncodeTiled failed for the tf32 contraction");
+      timed_launch(tf32 == 2 ? "layer_gemm_3xtf32" : "layer_gemm_tf32", stream, [&] {
+        kern<<<grid, tc::kThreads, smem, stream>>>(tmU, tmV, tmUl, tmVl, tmM, g.Cp, g.Kp, g.Tp, n * n);
       });
     } else {
       dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));

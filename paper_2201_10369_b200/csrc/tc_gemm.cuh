@@ -32,15 +32,25 @@
 namespace wino {
 namespace tc {
 
-constexpr int kM = 128, kN = 128, kBK = 32, kStages = 6;
+constexpr int kM = 128, kN = 128, kBK = 32;
 constexpr int kEpilogue = 128, kThreads = 64 + kEpilogue;
-constexpr int kAStage = kBK * kM * 4;   // 16 KB
-constexpr int kBStage = kBK * kN * 4;   // 16 KB
+constexpr int kAPlane = kBK * kM * 4;   // 16 KB: one operand plane of one stage
+constexpr int kBPlane = kBK * kN * 4;   // 16 KB
 constexpr int kStgBox = 32 * 32 * 4;                      // one epilogue TMA-store box
 constexpr int kStg = (kEpilogue / 32) * 2 * kStgBox;      // 4 warps x 2 buffers = 32 KB
-constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
-constexpr int kSmem = kStages * (kAStage + kBStage) + kStg + 1024 + kBarBytes;   // + alignment
 constexpr int kTmemCols = 2 * kN;
+// SPLIT = 1: 1xTF32 (operands TF32-rounded, one MMA per K = 8 step).  SPLIT = 3: 3xTF32
+// split precision: each operand x = hi + lo with hi = tf32(x), lo = tf32(x - hi), and
+// D += lo_A hi_B + hi_A lo_B + hi_A hi_B (small terms first), which recovers ~fp32 accuracy
+// at 3x the MMAs and 2x the operand bytes.
+template <int SPLIT>
+struct Cfg {
+  static constexpr int kPlanes = SPLIT == 1 ? 1 : 2;            // hi (+ lo) per operand
+  static constexpr int kAStage = kPlanes * kAPlane, kBStage = kPlanes * kBPlane;
+  static constexpr int kStages = SPLIT == 1 ? 6 : 3;            // 192 KB of operand ring either way
+  static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
+  static constexpr int kSmem = kStages * (kAStage + kBStage) + kStg + 1024 + kBarBytes;   // + alignment
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -114,12 +124,18 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 
 // M_p[k][t] = sum_c U_p[c][k] V_p[c][t] for p in [0, P); U [P][Cp][Kp], V [P][Cp][Tp],
 // M [P][Kp][Tp]; Cp % 32 == 0, Kp % 128 == 0, Tp % 128 == 0.  tmU / tmV: 2D tensor maps of
-// U as [P*Cp][Kp] and V as [P*Cp][Tp] (box 32 x 32, SWIZZLE_128B_ATOM_32B); tmM: M as
-// [P*Kp][Tp] (box 32 x 32, SWIZZLE_128B); see encode_map_2d.  Grid: <= one CTA per SM.
+// U as [P*Cp][Kp] and V as [P*Cp][Tp] (box 32 x 32, SWIZZLE_128B_ATOM_32B); tmUl / tmVl:
+// the same for the lo planes (SPLIT = 3 only); tmM: M as [P*Kp][Tp] (box 32 x 32,
+// SWIZZLE_128B); see encode_map_2d.  Grid: <= one CTA per SM.
+template <int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmU,
                                                                 const __grid_constant__ CUtensorMap tmV,
+                                                                const __grid_constant__ CUtensorMap tmUl,
+                                                                const __grid_constant__ CUtensorMap tmVl,
                                                                 const __grid_constant__ CUtensorMap tmM, int Cp, int Kp,
                                                                 long long Tp, int P) {
+  using C = Cfg<SPLIT>;
+  constexpr int kStages = C::kStages, kAStage = C::kAStage, kBStage = C::kBStage;
   extern __shared__ __align__(1024) unsigned char tsm[];
   const uint32_t raw = smem_u32(tsm);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -173,11 +189,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const __grid_con
           mbar_expect_tx(full0 + 8 * s, (uint32_t)(kAStage + kBStage));
           const int row = p * Cp + kt * kBK;
 #pragma unroll
-          for (int j = 0; j < kM / 32; j++)
+          for (int j = 0; j < kM / 32; j++) {
             tma_load_2d(a_base + s * kAStage + j * 4096, &tmU, kb * kM + 32 * j, row, full0 + 8 * s);
+            if (SPLIT == 3)
+              tma_load_2d(a_base + s * kAStage + kAPlane + j * 4096, &tmUl, kb * kM + 32 * j, row, full0 + 8 * s);
+          }
 #pragma unroll
-          for (int j = 0; j < kN / 32; j++)
+          for (int j = 0; j < kN / 32; j++) {
             tma_load_2d(b_base + s * kBStage + j * 4096, &tmV, tb * kN + 32 * j, row, full0 + 8 * s);
+            if (SPLIT == 3)
+              tma_load_2d(b_base + s * kBStage + kBPlane + j * 4096, &tmVl, tb * kN + 32 * j, row, full0 + 8 * s);
+          }
         }
       }
     }
@@ -200,7 +222,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const __grid_con
           for (int g = 0; g < kBK / 8; g++) {
             const uint64_t da = smem_desc(a_base + s * kAStage + g * 1024, 4096, 512);
             const uint64_t db = smem_desc(b_base + s * kBStage + g * 1024, 4096, 512);
-            mma_tf32(acc, da, db, (kt > 0 || g > 0) ? 1u : 0u);
+            if (SPLIT == 3) {
+              const uint64_t dal = smem_desc(a_base + s * kAStage + kAPlane + g * 1024, 4096, 512);
+              const uint64_t dbl = smem_desc(b_base + s * kBStage + kBPlane + g * 1024, 4096, 512);
+              mma_tf32(acc, dal, db, (kt > 0 || g > 0) ? 1u : 0u);
+              mma_tf32(acc, da, dbl, 1u);
+              mma_tf32(acc, da, db, 1u);
+            } else {
+              mma_tf32(acc, da, db, (kt > 0 || g > 0) ? 1u : 0u);
+            }
           }
           mma_commit(empty0 + 8 * s);
         }

@@ -31,11 +31,13 @@ def _run(x, w, pad, m, pts, flags, score=True):
     (2, 45, 37, 29, 130),       # C ragged over 32, K over 128, T = 2*19*15 = 570 over 256
     (3, 64, 40, 40, 256),
 ])
-def test_tf32_exact_on_representable_operands(N, C, H, W, K):
+@pytest.mark.parametrize("flags", [1, 2])
+def test_tf32_exact_on_representable_operands(N, C, H, W, K, flags):
+    """flags 1 = 1xTF32, 2 = 3xTF32 (whose lo planes are then exactly zero)."""
     x, w = synth.integer_layer_inputs(N, C, H, W, K, 3, lo=-3, hi=3, seed=21)
     y64 = ref.conv2d_direct64(x, w, 1)
     assert np.abs(y64).max() < 2 ** 20
-    y, s, mx = _run(x, w, 1, 2, OP.f23_c(1.0), flags=1)
+    y, s, mx = _run(x, w, 1, 2, OP.f23_c(1.0), flags=flags)
     assert np.array_equal(y.astype(np.float64), y64)
     assert s[0] == 0.0 and mx[0] == 0.0 and s[3] == y64.size
 
@@ -64,3 +66,23 @@ def test_tf32_error_bound(N, C, H, W, K, r, pad, m, pts):
     err0 = np.abs(ytf[:1].astype(np.float64) - y64).mean()
     assert 0.5 < err0 / maetf < 2.0
     print(f"\nm={m} r={r}: MAE fp32 {mae32:.3e}  tf32 {maetf:.3e}  ratio 2^{math.log2(maetf / mae32):.2f}")
+
+
+@pytest.mark.parametrize("N,C,H,W,K,r,pad,m,pts", [
+    (2, 256, 56, 56, 256, 3, 1, 6, OP.n8_cd(2.0, 1.003)),
+    (2, 128, 64, 64, 128, 5, 2, 4, OP.n8_c1c2(1.5, 3.1)),
+    (1, 45, 29, 37, 130, 3, 1, 4, OP.f43_c(1.622)),          # ragged C, K, T
+])
+def test_3xtf32_recovers_fp32_accuracy(N, C, H, W, K, r, pad, m, pts):
+    """3xTF32 (hi/lo split, three MMAs): the dropped lo*lo term is 2^-22 relative and the
+    fp32 accumulation matches the FFMA path's, so its MAE against fp64 direct is the fp32
+    path's within a factor 2 (vs 2^10 for 1xTF32), and its outputs stay within a few fp32
+    rounding errors of the parity path's."""
+    x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=3)
+    y32, s32, _ = _run(x, w, pad, m, pts, flags=0)
+    y3, s3, _ = _run(x, w, pad, m, pts, flags=2)
+    assert s3[3] == y3.size and s3[4] == 0
+    mae32, mae3 = s32[0] / s32[3], s3[0] / s3[3]
+    assert 0.5 * mae32 < mae3 < 2.0 * mae32
+    assert np.abs(y3 - y32).mean() < 2.0 * mae32
+    print(f"\nm={m} r={r}: MAE fp32 {mae32:.3e}  3xtf32 {mae3:.3e}")

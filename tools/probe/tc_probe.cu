@@ -21,7 +21,7 @@ int main(int argc, char** argv) {
   cudaMemcpy(dU, U.data(), U.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dV, V.data(), V.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(dM, 0xff, M.size() * 4);
-  cudaFuncSetAttribute((const void*)wino::tc::gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::kSmem);
+  cudaFuncSetAttribute((const void*)wino::tc::gemm_tf32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, wino::tc::Cfg<1>::kSmem);
   const int grid = argc > 5 ? atoi(argv[5]) : 148;   // persistent CTAs (fewer -> several tiles each)
   CUtensorMap tmU, tmV, tmM;
   const char* sw = getenv("TC_SWZ");
@@ -36,7 +36,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int rep = 0; rep < 4; rep++) {
     cudaEventRecord(e0);
-    wino::tc::gemm_tf32_kernel<<<grid, wino::tc::kThreads, wino::tc::kSmem>>>(tmU, tmV, tmM, Cp, Kp, Tp, 1);
+    wino::tc::gemm_tf32_kernel<1><<<grid, wino::tc::kThreads, wino::tc::Cfg<1>::kSmem>>>(tmU, tmV, tmU, tmV, tmM, Cp, Kp, Tp, 1);
     cudaEventRecord(e1);
   }
   cudaError_t e = cudaDeviceSynchronize();

@@ -13,7 +13,7 @@ def run(shape, m, pts, pad, reps=20):
     x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
     x, w = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
     out = {}
-    for flags in (0, 1):
+    for flags in (0, 1, 2):
         Ho = H + 2 * pad - r + 1
         y = torch.empty((N, K, Ho, Ho), device="cuda")
         ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, W, K, r, pad, m), dtype=torch.uint8, device="cuda")
@@ -27,14 +27,14 @@ def run(shape, m, pts, pad, reps=20):
             api.wino_conv2d_fp32(x, w, y, pad, m, pts, ws, flags=flags)
         e1.record(); torch.cuda.synchronize()
         fam = {f: api.wino_timing_read(f) for f in ("layer_filter", "layer_input", "layer_gemm",
-                                                   "layer_gemm_tf32", "layer_output")}
+                                                   "layer_gemm_tf32", "layer_gemm_3xtf32", "layer_output")}
         fam = {f: {"ms": v[0], "count": v[1]} for f, v in fam.items() if v[1]}
         api.wino_timing_enable(0)
         n = m + r - 1
         T = N * ((Ho + m - 1) // m) ** 2
         gemm_flop = 2.0 * n * n * C * K * T
-        g = fam.get("layer_gemm_tf32" if flags else "layer_gemm")
-        out["tf32" if flags else "fp32"] = {"ms": e0.elapsed_time(e1) / reps, "families": fam,
+        g = fam.get({0: "layer_gemm", 1: "layer_gemm_tf32", 2: "layer_gemm_3xtf32"}[flags])
+        out[{0: "fp32", 1: "tf32", 2: "3xtf32"}[flags]] = {"ms": e0.elapsed_time(e1) / reps, "families": fam,
                                             "gemm_tflops": gemm_flop / (g["ms"] / g["count"] * 1e-3) / 1e12 if g else None}
     return out
 
