@@ -187,16 +187,33 @@ def run_reference(args, rank, world):
 
 # ------------------------------------------------------------------ native arm
 
-def bench_layer(torch, dev, flush, steps=10):
-    """configs[2]: F(6x6,3x3) layer, N=32 C=K=256 56x56 pad 1, X16 points; unscored + scored."""
+def bench_layer(torch, dev, flush, steps=10, rank=0, world=1, dist=None):
+    """configs[2]: F(6x6,3x3) layer, N=32 C=K=256 56x56 pad 1, X16 points; unscored + scored.
+    With world > 1 the batch is sharded over the ranks: rank r runs images
+    [lo, hi); every timed iteration starts after a barrier and its time is the max over
+    ranks; scored statistics are all-reduced (SUM of sums, MAX of maxs)."""
     from paper_2201_10369_b200 import api, points as PP
+    from paper_2201_10369_b200.sweep import shard
     N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
     x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
-    xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
+    lo, hi = shard(N, rank, world)
+    Nr = hi - lo
+    xd, wd = torch.from_numpy(x[lo:hi]).to(dev), torch.from_numpy(w).to(dev)
     pts = PP.family_n8_cd(2.0, 1.003)
     Ho, Wo = H, W
-    y = torch.empty((N, K, Ho, Wo), dtype=torch.float32, device=dev)
-    ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, W, K, r, pad, m), dtype=torch.uint8, device=dev)
+    y = torch.empty((Nr, K, Ho, Wo), dtype=torch.float32, device=dev)
+    ws = torch.empty(api.wino_conv2d_workspace_bytes(Nr, C, H, W, K, r, pad, m), dtype=torch.uint8, device=dev)
+
+    def sync_ranks():
+        if world > 1:
+            dist.barrier(device_ids=[dev.index])
+
+    def max_over_ranks(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.cpu().tolist()
     sums = torch.zeros(5, dtype=torch.float64, device=dev)
     maxs = torch.zeros(2, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
@@ -209,6 +226,7 @@ def bench_layer(torch, dev, flush, steps=10):
     ts = []
     for _ in range(steps):
         flush()
+        sync_ranks()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
@@ -221,6 +239,7 @@ def bench_layer(torch, dev, flush, steps=10):
     sc = []
     for _ in range(2):
         flush()
+        sync_ranks()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sums, maxs)
@@ -233,6 +252,7 @@ def bench_layer(torch, dev, flush, steps=10):
         api.wino_timing_reset()
         for _ in range(steps):
             flush()
+            sync_ranks()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, flags=flag)
@@ -245,11 +265,17 @@ def bench_layer(torch, dev, flush, steps=10):
         mv = torch.zeros(2, dtype=torch.float64, device=dev)
         api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sv, mv, flags=flag)
         torch.cuda.synchronize()
-        return tv, kv, sv.cpu().numpy()
+        if world > 1:
+            dist.all_reduce(sv, op=dist.ReduceOp.SUM)
+        return max_over_ranks(tv), kv, sv.cpu().numpy()
 
     tf, kern_tf, s_tf = run_variant(api.WINO_CONV_TF32, "layer_gemm_tf32")
     tf3, kern_tf3, s_tf3 = run_variant(api.WINO_CONV_3XTF32, "layer_gemm_3xtf32")
     api.wino_timing_enable(False)
+    ts, sc = max_over_ranks(ts), max_over_ranks(sc)
+    if world > 1:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
     s = sums.cpu().numpy() / 2
     t = statistics.median(ts)
     direct_flop = 2.0 * N * K * C * Ho * Wo * r * r
@@ -293,6 +319,7 @@ def bench_layer(torch, dev, flush, steps=10):
     }
     return {
         "workload": "configs[2] F(6x6,3x3) N=32 C=K=256 56x56 pad 1, points {0,±2,±1/2,-1/1.003,1.003,inf}",
+        "parallelism": f"batch sharded over {world} ranks ({Nr} images on rank {rank}); time = max over ranks",
         "ms": t, "ms_min": min(ts), "effective_tflops": direct_flop / (t * 1e-3) / 1e12,
         "kernel_ms": kern, "flop_alg": f_alg, "bytes_alg": b_alg,
         "scored_ms": statistics.median(sc), "scored_mae": float(s[0] / s[3]) if s[3] else None,
@@ -309,7 +336,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--n-tiles", type=int, default=N_TILES)
-    ap.add_argument("--ref-every", type=int, default=32, help="oracle sample: every k-th candidate")
+    ap.add_argument("--ref-every", type=int, default=32, help="--impl reference: every k-th candidate per step")
+    ap.add_argument("--cpu-every", type=int, default=4,
+                    help="cpu_baseline sample: every k-th candidate (~12 s of host work at 16 cores)")
     ap.add_argument("--no-layer", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -461,9 +490,10 @@ def main():
                                  "min_mae": best, "n_nonfinite_candidates": int(np.sum(~np.isfinite(mae)))}
 
     layer = None
-    if rank == 0 and world == 1 and not args.no_layer:
-        layer, f_alg, b_alg, t_layer = bench_layer(torch, dev, flush)
-        t_roof = max(f_alg / (fp32_peak * 1e12), b_alg / (float(peaks.get("hbm_gbs", 6458.7)) * 1e9))
+    if not args.no_layer:
+        layer, f_alg, b_alg, t_layer = bench_layer(torch, dev, flush, rank=rank, world=world,
+                                                   dist=dist if world > 1 else None)
+        t_roof = max(f_alg / (fp32_peak * 1e12), b_alg / (float(peaks.get("hbm_gbs", 6458.7)) * 1e9)) / world
         layer["roofline_frac"] = t_roof / (t_layer * 1e-3)
         layer["roofline_bound"] = "fp32 FFMA (t_roof = max(F_alg/P_fp32, B_alg/BW_hbm))"
 
@@ -496,7 +526,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        evals_c, dt_c, thr, desc = oracle_sample_run(specs, args.ref_every)
+        evals_c, dt_c, thr, desc = oracle_sample_run(specs, args.cpu_every)
         cpu = {"value": evals_c / dt_c, "unit": "tile-evals/s", "cores": thr, "kind": "oracle", "sample": desc,
                "seconds": dt_c}
 
