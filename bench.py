@@ -497,7 +497,7 @@ def main():
         layer["roofline_frac"] = t_roof / (t_layer * 1e-3)
         layer["roofline_bound"] = "fp32 FFMA (t_roof = max(F_alg/P_fp32, B_alg/BW_hbm))"
 
-    # NEXT row N2: the Huffman-order variant of the configs[1] 2D uniform sweep, timed once
+    # NEXT row N2: the Huffman-order and mixed-precision variants of the configs[1] 2D sweep, timed once
     variants = None
     if rank == 0 and world == 1 and not args.no_layer:
         variants = {}
@@ -508,20 +508,24 @@ def main():
         hws = torch.empty(api.wino_error_sweep_workspace_bytes(2, 4, 3, S, T), dtype=torch.uint8, device=dev)
         hs = torch.zeros((S, 5), dtype=torch.float64, device=dev)
         hm = torch.zeros((S, 2), dtype=torch.float64, device=dev)
-        api.wino_error_sweep(2, 4, 3, sets, dd, gg, hs, hm, hws, flags=api.WINO_SWEEP_HUFFMAN)   # warm-up
-        flush()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        api.wino_error_sweep(2, 4, 3, sets, dd, gg, hs, hm, hws, flags=api.WINO_SWEEP_HUFFMAN)
-        b.record(stream)
-        b.synchronize()
-        hms = a.elapsed_time(b)
-        mae = curve(hs.cpu().numpy() / 2)
-        i, best = argmin_c(sp.spec.params, mae)
-        variants["huffman_2d"] = {
-            "workload": f"configs[1] 2D {sp.spec.dist} sweep ({S} c x {T} tiles), WINO_SWEEP_HUFFMAN (reading R21)",
-            "ms": hms, "value": S * T / (hms * 1e-3), "unit": "tile-evals/s",
-            "argmin_c": float(sp.spec.params[i]) if i is not None else None, "min_mae": best}
+        for vname, vflag, note in (("huffman_2d", api.WINO_SWEEP_HUFFMAN, "WINO_SWEEP_HUFFMAN (reading R21)"),
+                                   ("mixed_2d", api.WINO_SWEEP_MIXED, "WINO_SWEEP_MIXED (reading R22)")):
+            hs.zero_()
+            hm.zero_()
+            api.wino_error_sweep(2, 4, 3, sets, dd, gg, hs, hm, hws, flags=vflag)   # warm-up
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            api.wino_error_sweep(2, 4, 3, sets, dd, gg, hs, hm, hws, flags=vflag)
+            b.record(stream)
+            b.synchronize()
+            hms = a.elapsed_time(b)
+            mae = curve(hs.cpu().numpy() / 2)
+            i, best = argmin_c(sp.spec.params, mae)
+            variants[vname] = {
+                "workload": f"configs[1] 2D {sp.spec.dist} sweep ({S} c x {T} tiles), {note}",
+                "ms": hms, "value": S * T / (hms * 1e-3), "unit": "tile-evals/s",
+                "argmin_c": float(sp.spec.params[i]) if i is not None else None, "min_mae": best}
         del hws
 
     cpu = None

@@ -62,6 +62,12 @@ typedef enum {
  * Hadamard product RN(u*v).  Overrides WINO_SWEEP_NOFMA.  Compiled for F(2,3), F(4,3),
  * F(6,3) in 1D and 2D; other shapes return WINO_E_UNSUPPORTED. */
 #define WINO_SWEEP_HUFFMAN 2u
+/* Mixed precision ("double precision floating point for the transforms and single
+ * precision for Hadamard product"; reading R22): the transforms in fp64 with the
+ * fp64 (R64) matrices (ascending fma chains), U and V rounded to fp32, M = RN32(u*v), the
+ * output transform in fp64 rounded to fp32.  Compiled for F(2,3), F(4,3), F(6,3) in 1D and
+ * 2D; cannot be combined with WINO_SWEEP_HUFFMAN (WINO_E_INVALID_ARG). */
+#define WINO_SWEEP_MIXED 4u
 
 const char* wino_status_string(int status);
 const char* wino_last_error(void);

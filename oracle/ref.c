@@ -10,6 +10,10 @@
  *     products RN(a_j*b_j) of the non-zero matrix coefficients summed along a Huffman
  *     tree over the coefficient magnitudes |a_j| (reading R21);
  *     2D passes: left product first, then right (reading R8);
+ *   - the mixed-precision variant ("double precision floating point for the transforms
+ *     and single precision for Hadamard product"; reading R22): the three
+ *     transforms in fp64 with the fp64 (R64) matrices, each an ascending fma() chain, U and V
+ *     rounded to fp32, M = RN32(u*v), Y rounded to fp32;
  *   - fp64 direct valid cross-correlation of the same fp32 data (eq:conv P:112; O7);
  *   - error statistics of y32 against y64 ("L1 norm ... normal convolution using
  *     double precision"; O8);
@@ -135,6 +139,55 @@ static void tile_2d(int m, int r, const float* AT, const float* G, const float* 
   output_2d(m, n, AT, Mw, nofma, y);
 }
 
+/* ---------------------------------------------------------------- mixed precision (R22) */
+
+static double dot64(const double* a, int as, const double* x, int xs, int len) {
+  double acc = 0.0;
+  for (int j = 0; j < len; j++) acc = fma(a[j * as], x[j * xs], acc);
+  return acc;
+}
+
+/* 1D: U = RN32(G g), V = RN32(Bᵀ d) in fp64; M = RN32(U V); y = RN32(Aᵀ M) in fp64. */
+static void tile_mixed_1d(int m, int r, const double* AT, const double* G, const double* BT,
+                          const float* d, const float* g, float* y) {
+  const int n = m + r - 1;
+  double gd[OMAXN], dd[OMAXN], M[OMAXN];
+  for (int j = 0; j < r; j++) gd[j] = g[j];
+  for (int j = 0; j < n; j++) dd[j] = d[j];
+  for (int i = 0; i < n; i++) {
+    const float u = (float)dot64(G + i * r, 1, gd, 1, r);
+    const float v = (float)dot64(BT + i * n, 1, dd, 1, n);
+    M[i] = (double)(u * v);
+  }
+  for (int p = 0; p < m; p++) y[p] = (float)dot64(AT + p * n, 1, M, 1, n);
+}
+
+/* 2D: T1 = G g, U = RN32(T1 Gᵀ); T2 = Bᵀ d, V = RN32(T2 B); M = RN32(U ⊙ V);
+ * T3 = Aᵀ M, Y = RN32(T3 A); T1, T2, T3 in fp64, left product first (R8). */
+static void tile_mixed_2d(int m, int r, const double* AT, const double* G, const double* BT,
+                          const float* d, const float* g, float* y) {
+  const int n = m + r - 1;
+  double gd[OMAXN * OMAXN], dd[OMAXN * OMAXN], T[OMAXN * OMAXN], M[OMAXN * OMAXN];
+  float U[OMAXN * OMAXN];
+  for (int i = 0; i < r * r; i++) gd[i] = g[i];
+  for (int i = 0; i < n * n; i++) dd[i] = d[i];
+  for (int i = 0; i < n; i++)
+    for (int q = 0; q < r; q++) T[i * r + q] = dot64(G + i * r, 1, gd + q, r, r);
+  for (int i = 0; i < n; i++)
+    for (int l = 0; l < n; l++) U[i * n + l] = (float)dot64(G + l * r, 1, T + i * r, 1, r);
+  for (int i = 0; i < n; i++)
+    for (int q = 0; q < n; q++) T[i * n + q] = dot64(BT + i * n, 1, dd + q, n, n);
+  for (int i = 0; i < n; i++)
+    for (int l = 0; l < n; l++) {
+      const float v = (float)dot64(BT + l * n, 1, T + i * n, 1, n);
+      M[i * n + l] = (double)(U[i * n + l] * v);
+    }
+  for (int p = 0; p < m; p++)
+    for (int l = 0; l < n; l++) T[p * n + l] = dot64(AT + p * n, 1, M + l, n, n);
+  for (int p = 0; p < m; p++)
+    for (int s = 0; s < m; s++) y[p * m + s] = (float)dot64(AT + s * n, 1, T + p * n, 1, n);
+}
+
 /* fp64 direct valid cross-correlation of one tile (O7): products of two fp32 are exact in
  * fp64; summation ascending u then v. */
 static void direct64_tile(int dims, int m, int r, const float* d, const float* g, double* y) {
@@ -245,6 +298,42 @@ int oref_sweep(int dims, int m, int r, int n_cand, const float* mats, int64_t n_
       if (direct32) direct32_tile(dims, m, r, d, g, nofma, y);
       else if (dims == 1) tile_1d(m, r, AT, G, BT, d, g, nofma, y);
       else tile_2d(m, r, AT, G, BT, d, g, nofma, y);
+      for (int o = 0; o < dy; o++) stat_acc(su, mx, y[o], y64[t * dy + o]);
+      if (y_dump && t < n_dump)
+        memcpy(y_dump + ((int64_t)s * n_dump + t) * dy, y, sizeof(float) * dy);
+    }
+  }
+  free(y64);
+  return 0;
+}
+
+/* O9 for the mixed-precision variant: mats64 per candidate [AT | G | BT] fp64 (R64);
+ * otherwise as oref_sweep (sums/maxs OVERWRITTEN, optional y_dump). */
+int oref_sweep_mixed(int dims, int m, int r, int n_cand, const double* mats64, int64_t n_tiles,
+                     const float* d_tiles, const float* g_tiles, double* sums, double* maxs,
+                     int64_t n_dump, float* y_dump) {
+  const int n = m + r - 1;
+  if (m < 1 || r < 1 || n > OMAXN || (dims != 1 && dims != 2)) return 1;
+  const int dn = dims == 1 ? n : n * n, dg = dims == 1 ? r : r * r, dy = dims == 1 ? m : m * m;
+  const int64_t mstride = (int64_t)m * n + (int64_t)n * r + (int64_t)n * n;
+  double* y64 = (double*)malloc(sizeof(double) * (size_t)(n_tiles > 0 ? n_tiles : 1) * dy);
+  if (!y64) return 2;
+  oref_direct64_tiles(dims, m, r, n_tiles, d_tiles, g_tiles, y64);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int s = 0; s < n_cand; s++) {
+    const double* AT = mats64 + s * mstride;
+    const double* G = AT + m * n;
+    const double* BT = G + n * r;
+    double* su = sums + 5 * (int64_t)s;
+    double* mx = maxs + 2 * (int64_t)s;
+    for (int i = 0; i < 5; i++) su[i] = 0.0;
+    mx[0] = mx[1] = 0.0;
+    float y[OMAXN * OMAXN];
+    for (int64_t t = 0; t < n_tiles; t++) {
+      const float* d = d_tiles + t * dn;
+      const float* g = g_tiles + t * dg;
+      if (dims == 1) tile_mixed_1d(m, r, AT, G, BT, d, g, y);
+      else tile_mixed_2d(m, r, AT, G, BT, d, g, y);
       for (int o = 0; o < dy; o++) stat_acc(su, mx, y[o], y64[t * dy + o]);
       if (y_dump && t < n_dump)
         memcpy(y_dump + ((int64_t)s * n_dump + t) * dy, y, sizeof(float) * dy);

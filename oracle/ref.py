@@ -46,6 +46,7 @@ def lib():
                                        + [ctypes.c_int] * 3)
         L.oref_conv2d_direct64.argtypes = [_f, _f, _d] + [ctypes.c_int] * 9
         L.oref_stats.argtypes = [_f, _d, _i64, _d, _d]
+        L.oref_sweep_mixed.argtypes = ([ctypes.c_int] * 4 + [_d, _i64, _f, _f, _d, _d, _i64, _f])
         L.oref_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -105,6 +106,32 @@ def sweep(dims, m, r, point_sets, d_tiles, g_tiles, nofma=False, n_dump=0, mats=
     if mats is None:
         mats = pack_mats(m, r, point_sets)
     return _sweep(dims, m, r, mats, d_tiles, g_tiles, _mode(nofma, huffman), False, n_dump)
+
+
+def pack_mats64(m: int, r: int, point_sets: Sequence[Sequence[float]]) -> np.ndarray:
+    """[n_cand, m*n + n*r + n*n] fp64: the R64 matrices, per candidate."""
+    rows = []
+    for pts in point_sets:
+        AT, G, BT = r64.build_r64(m, r, pts)
+        rows.append(np.concatenate([np.asarray(AT).ravel(), np.asarray(G).ravel(), np.asarray(BT).ravel()]))
+    return np.ascontiguousarray(np.stack(rows), dtype=np.float64)
+
+
+def sweep_mixed(dims, m, r, point_sets, d_tiles, g_tiles, n_dump=0):
+    """O9 for the mixed-precision variant (reading R22): fp64 transforms with the R64
+    matrices, fp32 U, V and Hadamard product, fp32 output.  Returns (sums, maxs, y_dump)."""
+    mats = pack_mats64(m, r, point_sets)
+    d_tiles, g_tiles = _c32(d_tiles), _c32(g_tiles)
+    S, nt = mats.shape[0], d_tiles.shape[0]
+    sums = np.zeros((S, 5))
+    maxs = np.zeros((S, 2))
+    ydump = np.zeros((S, n_dump, m ** dims), dtype=np.float32) if n_dump else None
+    rc = lib().oref_sweep_mixed(dims, m, r, S, _p(mats, ctypes.c_double), nt, _p(d_tiles, ctypes.c_float),
+                                _p(g_tiles, ctypes.c_float), _p(sums, ctypes.c_double), _p(maxs, ctypes.c_double),
+                                int(n_dump), _p(ydump, ctypes.c_float))
+    if rc:
+        raise ValueError("oref_sweep_mixed failed")
+    return sums, maxs, ydump
 
 
 def direct32_sweep(dims, m, r, d_tiles, g_tiles, nofma=True):

@@ -16,6 +16,7 @@ WINO_SUMS = 5
 WINO_MAXS = 2
 WINO_SWEEP_NOFMA = 1
 WINO_SWEEP_HUFFMAN = 2
+WINO_SWEEP_MIXED = 4
 WINO_CONV_TF32 = 1
 WINO_CONV_3XTF32 = 2
 WINO_MAX_N = 16

@@ -200,7 +200,10 @@ static int sweep_common(int dims, int m, int r, const double* point_sets, int n_
   if (n_cand > 0 && (!point_sets || !cand_status)) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (n_cand > 0 && n_tiles > 0 && (!d_tiles || !g_tiles)) return set_error(WINO_E_INVALID_ARG, "NULL tiles");
   if (!d_y && n_cand > 0 && (!d_sums || !d_maxs)) return set_error(WINO_E_INVALID_ARG, "NULL stats");
-  if (flags & ~(WINO_SWEEP_NOFMA | WINO_SWEEP_HUFFMAN)) return set_error(WINO_E_INVALID_ARG, "unknown flags");
+  if (flags & ~(WINO_SWEEP_NOFMA | WINO_SWEEP_HUFFMAN | WINO_SWEEP_MIXED))
+    return set_error(WINO_E_INVALID_ARG, "unknown flags");
+  if ((flags & WINO_SWEEP_HUFFMAN) && (flags & WINO_SWEEP_MIXED))
+    return set_error(WINO_E_INVALID_ARG, "WINO_SWEEP_HUFFMAN and WINO_SWEEP_MIXED are exclusive");
   const int n = m + r - 1;
   if (n > WINO_MAX_N) return set_error(WINO_E_UNSUPPORTED, "n > WINO_MAX_N");
   if (!sweep_supported(dims, m, r))

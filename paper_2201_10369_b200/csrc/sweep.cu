@@ -36,6 +36,7 @@
 #include <cmath>
 
 #include "sweep_huff.cuh"
+#include "sweep_mixed.cuh"
 
 namespace wino {
 
@@ -118,6 +119,13 @@ const std::vector<SweepCfg>& cfgs() {
 
 const HuffCfg* find_huff(int dims, int m, int r) {
   static const std::vector<HuffCfg> v = sweep_huff_cfgs();
+  for (const auto& h : v)
+    if (h.dims == dims && h.m == m && h.r == r) return &h;
+  return nullptr;
+}
+
+const HuffCfg* find_mixed(int dims, int m, int r) {
+  static const std::vector<HuffCfg> v = sweep_mixed_cfgs();
   for (const auto& h : v)
     if (h.dims == dims && h.m == m && h.r == r) return &h;
   return nullptr;
@@ -213,8 +221,8 @@ WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
     const long long nb = std::max(n_tblk_of(c.dims, lay, n_tiles), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }
-  {  // Huffman kernels: tile pairs, 2 * kSwThreads tiles per block
-    const long long nb = std::max((long long)((n_tiles + 2 * kSwThreads - 1) / (2 * kSwThreads)), 1LL);
+  for (long long tpb : {2LL * kSwThreads, (long long)kSwThreads}) {   // Huffman / mixed kernels
+    const long long nb = std::max((long long)((n_tiles + tpb - 1) / tpb), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }
   const long long n_ref_blocks = (n_tiles + 255) / 256;
@@ -252,18 +260,24 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   const bool dump = d_y != nullptr;
   const bool huff = (flags & WINO_SWEEP_HUFFMAN) != 0;
   const int nofma = (flags & WINO_SWEEP_NOFMA) ? 1 : 0;
-  const HuffCfg* hc = huff ? find_huff(dims, m, r) : nullptr;
-  if (huff && !hc)
-    return set_error(WINO_E_UNSUPPORTED, "no Huffman-order sweep kernel for dims=%d m=%d r=%d", dims, m, r);
+  const bool mixed = (flags & WINO_SWEEP_MIXED) != 0;
+  const HuffCfg* hc = huff ? find_huff(dims, m, r) : mixed ? find_mixed(dims, m, r) : nullptr;
+  if ((huff || mixed) && !hc)
+    return set_error(WINO_E_UNSUPPORTED, "no %s sweep kernel for dims=%d m=%d r=%d",
+                     huff ? "Huffman-order" : "mixed-precision", dims, m, r);
   const std::vector<Variant>& variants = c->variants;
   const Layout lay = variants.back().lay[nofma];
   const int n = m + r - 1;
   const int per = per_cand(m, r);
-  const int stride = huff ? per + huff_prog_words(m, r) : per;   // floats per candidate in the params
-  int cmax = huff ? std::min(kParamFloats / stride, kMaxCandsLaunch) : sweep_max_cands_per_launch(dims, m, r);
+  // floats per candidate in the params: Huffman = matrices + programs, mixed = fp64 matrices
+  const int stride = huff ? per + huff_prog_words(m, r) : mixed ? 2 * per : per;
+  int cmax = (huff || mixed) ? std::min(kParamFloats / stride, kMaxCandsLaunch)
+                             : sweep_max_cands_per_launch(dims, m, r);
   const int dy = dims == 1 ? m : m * m;
-  const long long tpb_h = 2 * kSwThreads;
-  const long long n_tblk = n_tiles <= 0 ? 0 : huff ? (n_tiles + tpb_h - 1) / tpb_h : n_tblk_of(dims, lay, n_tiles);
+  const long long tpb_h = huff ? 2 * kSwThreads : kSwThreads;   // tiles per block, Huffman / mixed
+  const long long n_tblk = n_tiles <= 0 ? 0
+                           : (huff || mixed) ? (n_tiles + tpb_h - 1) / tpb_h
+                                             : n_tblk_of(dims, lay, n_tiles);
   const int tpc = tblk_per_cta(std::max(n_tblk, 1LL));
   const int n_tg = (int)((n_tblk + tpc - 1) / tpc);
   const bool work = n_tiles > 0 && n_cand > 0;
@@ -278,15 +292,16 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   double* partial = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.partial);
   double* ref_part = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_part);
   double* ref_tot = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_tot);
-  const size_t smem = huff ? (size_t)(2 * n - 1) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
-                                 (size_t)kMaxCpc * 4 * kPartial * 8
-                           : smem_bytes(dims, m, r, lay);
-  if (work && huff && smem > 48 * 1024) {
+  const size_t smem = huff    ? (size_t)(2 * n - 1) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
+                                    (size_t)kMaxCpc * 4 * kPartial * 8
+                      : mixed ? (size_t)dy * kSwThreads * 8 + (size_t)kMaxCpc * 4 * kPartial * 8
+                              : smem_bytes(dims, m, r, lay);
+  if (work && (huff || mixed) && smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute((const void*)hc->k[dump ? 1 : 0],
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   }
-  if (work && !huff && smem > 48 * 1024) {
+  if (work && !huff && !mixed && smem > 48 * 1024) {
     for (const Variant& v : variants) {
       cudaError_t e = cudaFuncSetAttribute((const void*)v.k[nofma][dump ? 1 : 0],
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -333,6 +348,12 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
           dst[m * n + n * r + t] = (float)BT[t];
           if (dst[m * n + n * r + t] != 0.0f) nzB |= t < 64 ? 1ull << t : ~0ull;
         }
+        if (mixed) {   // the fp64 matrices themselves (R64, not rounded)
+          double* d64 = reinterpret_cast<double*>(dst);
+          std::copy(AT, AT + m * n, d64);
+          std::copy(G, G + n * r, d64 + m * n);
+          std::copy(BT, BT + n * n, d64 + m * n + n * r);
+        }
         if (huff) {   // programs after the matrices: G rows, Bᵀ rows, Aᵀ rows
           unsigned char* pr = reinterpret_cast<unsigned char*>(dst + per);
           std::fill(pr, pr + 4 * huff_prog_words(m, r), (unsigned char)0);
@@ -367,7 +388,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
         var = &v;
         break;
       }
-    SweepKernel kern = huff ? hc->k[dump ? 1 : 0] : var->k[nofma][dump ? 1 : 0];
+    SweepKernel kern = (huff || mixed) ? hc->k[dump ? 1 : 0] : var->k[nofma][dump ? 1 : 0];
     // Work item = (up to cpc candidates, one tile group).  Persistent grid of one wave of
     // resident CTAs walking the items round-robin; cpc is chosen (<= kMaxCpc, larger is
     // better for amortising the tile loads) so the items fill whole rounds of the wave.
@@ -401,7 +422,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     args.n_tgroups = n_tg;
     args.n_cgroups = groups;
     dim3 grid((unsigned)std::min<long long>(n_items, slots));
-    timed_launch(huff ? "sweep_huffman" : dims == 1 ? "sweep1d" : "sweep2d", stream,
+    timed_launch(huff ? "sweep_huffman" : mixed ? "sweep_mixed" : dims == 1 ? "sweep1d" : "sweep2d", stream,
                  [&] { kern<<<grid, kSwThreads, smem, stream>>>(args, *P, *DI); });
     launches++;
     cudaError_t e = cudaGetLastError();

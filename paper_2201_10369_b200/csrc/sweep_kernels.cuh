@@ -954,7 +954,7 @@ inline constexpr uint64_t kF43A = 0x124920ull, kF43G = 0x18180ull, kF43B = 0x561
 inline constexpr uint64_t kF23A = 0x28ull, kF23G = 0x630ull, kF23B = 0x59a9ull;
 
 
-// Huffman-order sweep kernels (sweep_huff.cuh), [dump]
+// Huffman-order (sweep_huff.cuh) and mixed-precision (sweep_mixed.cuh) sweep kernels, [dump]
 struct HuffCfg {
   int dims, m, r;
   SweepKernel k[2];
@@ -967,5 +967,6 @@ std::vector<SweepCfg> sweep_cfgs_2d_f43();
 std::vector<SweepCfg> sweep_cfgs_2d_small();
 std::vector<SweepCfg> sweep_cfgs_2d_large();
 std::vector<HuffCfg> sweep_huff_cfgs();
+std::vector<HuffCfg> sweep_mixed_cfgs();
 
 }  // namespace wino

@@ -320,3 +320,72 @@ def test_huffman_reproduces_paper_f43_rows(dims):
         assert 0.97 <= eh[j] / paper <= 1.05, (j, eh[j], paper)
         assert abs(eh[j] / paper - 1) < abs(es[j] / paper - 1)
     assert eh[0] < eh[1]
+
+
+# ------------------------------------------------------------------ N2: mixed precision (R22)
+
+def test_mixed_exact_special_case():
+    """fp64 transforms on integer tiles with F(2,3) {0,±1,∞}: every value is exact, so the
+    mixed-precision output is the exact correlation."""
+    d, g = synth.integer_tiles(200, 2, 4, 3, seed=6)
+    _, _, y = ref.sweep_mixed(2, 2, 3, [P.f23_c(1.0)], d, g, n_dump=200)
+    for t in range(0, 200, 23):
+        ex = exact.correlate_2d(d[t].reshape(4, 4).astype(int).tolist(), g[t].reshape(3, 3).astype(int).tolist())
+        assert y[0, t].reshape(2, 2).tolist() == [[float(v) for v in row] for row in ex]
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+def test_mixed_error_bound(dims):
+    """R22 leaves three fp32 roundings per Winograd-domain term (U, V, U*V) and one on the
+    output: |y - y64| <= u|y64| + 3.01 u Σ|A||A| |U V| (+ fp64 noise), u = 2^-24, with U, V
+    the exact-transform values (fp64 from the R64 matrices); the bound holds for every
+    output, and the mixed mode beats the all-fp32 mode on average."""
+    c = 1.829 if dims == 1 else 1.622
+    pts = P.f43_c(c)
+    d, g = synth.random_tiles(2000, dims, 6, 3, "uniform", seed=8)
+    _, _, ym = ref.sweep_mixed(dims, 4, 3, [pts], d, g, n_dump=2000)
+    _, _, yf = ref.sweep(dims, 4, 3, [pts], d, g, n_dump=2000)
+    y64 = ref.direct64_tiles(dims, 4, 3, d, g)
+    AT, G, BT = (np.asarray(M_, dtype=np.float64) for M_ in r64.build_r64(4, 3, pts))
+    u = 2.0 ** -24
+    if dims == 1:
+        U = g.astype(np.float64) @ G.T
+        V = d.astype(np.float64) @ BT.T
+        bound = u * np.abs(y64) + 3.01 * u * (np.abs(U * V) @ np.abs(AT).T) + 1e-12
+    else:
+        gg = g.reshape(-1, 3, 3).astype(np.float64)
+        dd = d.reshape(-1, 6, 6).astype(np.float64)
+        U = G @ gg @ G.T
+        V = BT @ dd @ BT.T
+        W_ = np.abs(U * V)
+        bound = (u * np.abs(y64).reshape(-1, 4, 4) + 3.01 * u * (np.abs(AT) @ W_ @ np.abs(AT).T) + 1e-12)
+        bound = bound.reshape(-1, 16)
+    em = np.abs(ym[0].astype(np.float64) - y64)
+    ef = np.abs(yf[0].astype(np.float64) - y64)
+    assert np.all(em <= bound)
+    assert em.mean() < ef.mean()
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+def test_mixed_reduces_to_rounded_exact_transforms(dims):
+    """With F(2,3) on {0,±1,∞} every fp64 transform of fp32 data is exact (coefficients 0,
+    ±1/2, ±1; at most 16 terms), so R22 reduces to: U, V = RN32(exact transforms),
+    M = RN32(U V), y = RN32(exact Aᵀ M A) -- three library roundings, computed here with
+    numpy float32 / float64 on the exact rational matrices of O2."""
+    pts = P.f23_c(1.0)
+    AT, G, BT = (np.asarray(M_, dtype=np.float64) for M_ in r64.build_r64(2, 3, pts))
+    for M_ in (AT, G, BT):                      # dyadic: the fp64 matrices are the exact ones
+        assert np.all(M_ * 2 == np.round(M_ * 2))
+    d, g = synth.random_tiles(3000, dims, 4, 3, "uniform", seed=9)
+    _, _, ym = ref.sweep_mixed(dims, 2, 3, [pts], d, g, n_dump=3000)
+    _, _, yf = ref.sweep(dims, 2, 3, [pts], d, g, n_dump=3000)
+    if dims == 1:
+        U = (g.astype(np.float64) @ G.T).astype(np.float32)
+        V = (d.astype(np.float64) @ BT.T).astype(np.float32)
+        y = ((U * V).astype(np.float64) @ AT.T).astype(np.float32)
+    else:
+        U = (G @ g.reshape(-1, 3, 3).astype(np.float64) @ G.T).astype(np.float32)
+        V = (BT @ d.reshape(-1, 4, 4).astype(np.float64) @ BT.T).astype(np.float32)
+        y = (AT @ (U * V).astype(np.float64) @ AT.T).astype(np.float32).reshape(-1, 4)
+    assert np.array_equal(ym[0], y)
+    assert not np.array_equal(yf[0], y)

@@ -1,4 +1,4 @@
-"""Time the Huffman-order sweep (NEXT row N2) on the configs[1] workload (4096 c x 100k
+"""Time the Huffman-order and mixed-precision sweeps (NEXT row N2) on the configs[1] workload (4096 c x 100k
 tiles, uniform) next to the production F32-FMA sweep; prints one JSON object."""
 import json
 import sys
@@ -19,7 +19,7 @@ for dims in (1, 2):
     dd, gg = torch.from_numpy(d).cuda(), torch.from_numpy(g).cuda()
     S, T = len(sets), d.shape[0]
     ws = torch.empty(api.wino_error_sweep_workspace_bytes(dims, 4, 3, S, T), dtype=torch.uint8, device="cuda")
-    for name, flags in (("fma", 0), ("nofma", 1), ("huffman", 2)):
+    for name, flags in (("fma", 0), ("nofma", 1), ("huffman", 2), ("mixed", 4)):
         sums = torch.zeros((S, 5), dtype=torch.float64, device="cuda")
         maxs = torch.zeros((S, 2), dtype=torch.float64, device="cuda")
         api.wino_error_sweep(dims, 4, 3, sets, dd, gg, sums, maxs, ws, flags=flags)
