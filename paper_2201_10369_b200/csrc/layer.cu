@@ -117,8 +117,8 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
 // ------------------------------------------------------------------ K2
 // one thread per (c, t); t fastest -> coalesced V stores per Winograd position
 template <int M, int R>
-__global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V, Geo geo,
-                             const __grid_constant__ LayerMats mt) {
+__global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(const float* __restrict__ x, float* __restrict__ V, Geo geo,
+                                                       const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp * Tp
   if (idx >= (long long)geo.Cp * geo.Tp) return;
@@ -268,8 +268,8 @@ using tc::gemm_tf32_kernel;
 // ------------------------------------------------------------------ K4
 // one thread per (k, t); t fastest -> coalesced M loads per Winograd position
 template <int M, int R>
-__global__ void output_kernel(const float* __restrict__ Mw, float* __restrict__ y, Geo geo,
-                              const __grid_constant__ LayerMats mt) {
+__global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(const float* __restrict__ Mw, float* __restrict__ y, Geo geo,
+                                                        const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * T
   if (idx >= (long long)geo.K * geo.T) return;
@@ -277,22 +277,23 @@ __global__ void output_kernel(const float* __restrict__ Mw, float* __restrict__ 
   const int k = (int)(idx / geo.T);
   const long long plane = (long long)geo.Kp * geo.Tp;
   const float* src = Mw + (long long)k * geo.Tp + t;
-  float mw[N][N];
-#pragma unroll
-  for (int i = 0; i < N; i++)
-#pragma unroll
-    for (int l = 0; l < N; l++) mw[i][l] = src[(i * N + l) * plane];
-  // T3[p][l] = Σ_i Aᵀ[p][i] Mw[i][l]
+  // T3[p][l] = Σ_i Aᵀ[p][i] Mw[i][l]: rows of Mw streamed in ascending i (each (p, l) is
+  // still one ascending fmaf chain from +0)
   float t3[M][N];
 #pragma unroll
   for (int p = 0; p < M; p++)
 #pragma unroll
-    for (int l = 0; l < N; l++) {
-      float acc = 0.0f;
+    for (int l = 0; l < N; l++) t3[p][l] = 0.0f;
 #pragma unroll
-      for (int i = 0; i < N; i++) acc = __fmaf_rn(mt.AT[p * N + i], mw[i][l], acc);
-      t3[p][l] = acc;
-    }
+  for (int i = 0; i < N; i++) {
+    float mw[N];
+#pragma unroll
+    for (int l = 0; l < N; l++) mw[l] = src[(i * N + l) * plane];
+#pragma unroll
+    for (int p = 0; p < M; p++)
+#pragma unroll
+      for (int l = 0; l < N; l++) t3[p][l] = __fmaf_rn(mt.AT[p * N + i], mw[l], t3[p][l]);
+  }
   const int per_img = geo.th * geo.tw;
   const int img = (int)(t / per_img);
   const int rem = (int)(t - (long long)img * per_img);
