@@ -299,16 +299,32 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
   const int rem = (int)(t - (long long)img * per_img);
   const int ty = rem / geo.tw, tx = rem - ty * geo.tw;
   float* yk = y + ((long long)img * geo.K + k) * geo.Ho * geo.Wo;
+  // rows of the output tile; even M with an even row length -> 8-byte pair stores (the
+  // lanes of a warp cover consecutive tiles, so a pair store fills 1/3 of a 768 B span
+  // instead of 1/6)
+  const bool pairs = (M % 2 == 0) && (geo.Wo % 2 == 0) && (reinterpret_cast<uintptr_t>(y) % 8 == 0);
 #pragma unroll
   for (int p = 0; p < M; p++) {
     const int h = ty * M + p;
+    float yr[M];
 #pragma unroll
     for (int s = 0; s < M; s++) {
       float acc = 0.0f;
 #pragma unroll
       for (int l = 0; l < N; l++) acc = __fmaf_rn(t3[p][l], mt.AT[s * N + l], acc);
-      const int ww = tx * M + s;
-      if (h < geo.Ho && ww < geo.Wo) yk[(long long)h * geo.Wo + ww] = acc;
+      yr[s] = acc;
+    }
+    if (h >= geo.Ho) continue;
+    float* row = yk + (long long)h * geo.Wo + tx * M;
+    const int wmax = geo.Wo - tx * M;   // valid columns in this tile row
+    if (pairs) {
+#pragma unroll
+      for (int s = 0; s + 1 < M; s += 2)
+        if (s < wmax) *reinterpret_cast<float2*>(row + s) = make_float2(yr[s], yr[s + 1]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < M; s++)
+        if (s < wmax) row[s] = yr[s];
     }
   }
 }
