@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
       for (int j = 0; j < N; j++) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
       t2[i][q] = acc;
     }
-  // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
+  // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]; positions p = i N + l are stored in ascending order
+  // through a running pointer (one 64-bit add per store instead of a full address product)
+  float* dst = V + idx;
+  const long long lo_off = (long long)N * N * plane;   // 3xTF32 lo planes
 #pragma unroll
   for (int i = 0; i < N; i++)
 #pragma unroll
@@ -165,11 +168,12 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
       for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
       if (geo.tf32 == 2) {
         const float hi = round_tf32(acc);
-        V[(i * N + l) * plane + idx] = hi;
-        V[(N * N + i * N + l) * plane + idx] = round_tf32(acc - hi);
+        dst[0] = hi;
+        dst[lo_off] = round_tf32(acc - hi);
       } else {
-        V[(i * N + l) * plane + idx] = geo.tf32 ? round_tf32(acc) : acc;
+        dst[0] = geo.tf32 ? round_tf32(acc) : acc;
       }
+      dst += plane;
     }
 }
 
@@ -523,6 +527,25 @@ struct WsLayout {
   size_t u_off, v_off, m_off, p_off, total;
 };
 
+// per-thread, per-device side stream + fork/join events for layer_launch
+struct SideStream {
+  bool ok = false;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  thread_local SideStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& ss = per_dev[dev & 63];
+  if (!ss.ok && ss.s == nullptr) {
+    ss.ok = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) == cudaSuccess;
+  }
+  return ss;
+}
+
 WsLayout ws_layout(const Geo& g) {
   const int n = g.m + g.r - 1, nn = n * n;
   WsLayout L;
@@ -599,19 +622,28 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   double* partial = reinterpret_cast<double*>(ws + L.p_off);
   const int tpb = 256;
   int launches = 0;
+  // K1 (filter) and K2 (input) are independent: K1 runs on a per-thread, per-device side
+  // stream forked from / joined to `stream` with events (graph-capture compatible), so the
+  // small filter transform hides under the input transform.
+  SideStream& side = side_stream();
+  bool forked = side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
+                cudaStreamWaitEvent(side.s, side.fork, 0) == cudaSuccess;
+  cudaStream_t fs = forked ? side.s : stream;
   {
     const long long tot = (long long)g.Cp * g.Kp;
     const auto fk = cfg->fk;
-    timed_launch("layer_filter", stream,
-                 [&] { fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(w, U, C, K, g.Cp, g.Kp, g.tf32, mt); });
+    timed_launch("layer_filter", fs,
+                 [&] { fk<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, fs>>>(w, U, C, K, g.Cp, g.Kp, g.tf32, mt); });
     launches++;
   }
+  if (forked) cudaEventRecord(side.join, fs);
   {
     const long long tot = (long long)g.Cp * g.Tp;
     const auto ik = cfg->ik;
     timed_launch("layer_input", stream, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt); });
     launches++;
   }
+  if (forked) cudaStreamWaitEvent(stream, side.join, 0);
   {
     if (tf32) {
       static bool tattr[2] = {false, false};
