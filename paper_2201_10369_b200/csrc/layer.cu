@@ -115,66 +115,89 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
 }
 
 // ------------------------------------------------------------------ K2
-// one thread per (c, t); t fastest -> coalesced V stores per Winograd position
+// one thread per (kInCpt channels, t); t fastest -> coalesced V stores per Winograd
+// position.  The tile geometry, padding predicates and patch offsets are computed once and
+// reused for the thread's kInCpt channels (the kernel is issue-bound on that arithmetic).
+// channels per thread: 4 for the large n = 10 tiles (where the per-tile arithmetic
+// dominates), 1 otherwise (more threads in flight); always divides Cp (a multiple of 16)
+template <int N>
+constexpr int in_cpt() { return N > 8 ? 4 : 1; }
 template <int M, int R>
 __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(const float* __restrict__ x, float* __restrict__ V, Geo geo,
                                                        const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp * Tp
-  if (idx >= (long long)geo.Cp * geo.Tp) return;
-  const long long t = idx % geo.Tp;
-  const int c = (int)(idx / geo.Tp);
+  constexpr int kInCpt = in_cpt<N>();
+  static_assert(N <= 16, "row / column masks are 16 bits");
+  const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp / kInCpt * Tp
+  if (gidx >= (long long)(geo.Cp / kInCpt) * geo.Tp) return;
+  const long long t = gidx % geo.Tp;
+  const int c0 = (int)(gidx / geo.Tp) * kInCpt;
   const long long plane = (long long)geo.Cp * geo.Tp;
-  if (t >= geo.T || c >= geo.C) {
-#pragma unroll
-    for (int p = 0; p < (geo.tf32 == 2 ? 2 : 1) * N * N; p++) V[p * plane + idx] = 0.0f;
-    return;
-  }
-  const int per_img = geo.th * geo.tw;
-  const int img = (int)(t / per_img);
-  const int rem = (int)(t - (long long)img * per_img);
-  const int ty = rem / geo.tw, tx = rem - ty * geo.tw;
-  const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
-  const int h0 = ty * M - geo.pad, w0 = tx * M - geo.pad;
-  float d[N][N];
-#pragma unroll
-  for (int a = 0; a < N; a++)
-#pragma unroll
-    for (int b = 0; b < N; b++) {
-      const int h = h0 + a, ww = w0 + b;
-      d[a][b] = (h >= 0 && h < geo.H && ww >= 0 && ww < geo.W) ? __ldg(xc + (long long)h * geo.W + ww) : 0.0f;
-    }
-  // T2[i][q] = Σ_j Bᵀ[i][j] d[j][q]
-  float t2[N][N];
-#pragma unroll
-  for (int q = 0; q < N; q++)
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int j = 0; j < N; j++) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
-      t2[i][q] = acc;
-    }
-  // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]; positions p = i N + l are stored in ascending order
-  // through a running pointer (one 64-bit add per store instead of a full address product)
-  float* dst = V + idx;
   const long long lo_off = (long long)N * N * plane;   // 3xTF32 lo planes
+  const bool tile_ok = t < geo.T;
+  int img = 0, h0 = 0, w0 = 0;
+  unsigned rowm = 0, colm = 0;
+  if (tile_ok) {
+    const int per_img = geo.th * geo.tw;
+    img = (int)(t / per_img);
+    const int rem = (int)(t - (long long)img * per_img);
+    const int ty = rem / geo.tw, tx = rem - ty * geo.tw;
+    h0 = ty * M - geo.pad;
+    w0 = tx * M - geo.pad;
 #pragma unroll
-  for (int i = 0; i < N; i++)
+    for (int a = 0; a < N; a++) rowm |= (h0 + a >= 0 && h0 + a < geo.H) ? 1u << a : 0u;
 #pragma unroll
-    for (int l = 0; l < N; l++) {
-      float acc = 0.0f;
+    for (int b = 0; b < N; b++) colm |= (w0 + b >= 0 && w0 + b < geo.W) ? 1u << b : 0u;
+  }
+  const long long off0 = (long long)h0 * geo.W + w0;   // patch origin (may lie outside)
+#pragma unroll 1
+  for (int cc = 0; cc < kInCpt; cc++) {
+    const int c = c0 + cc;
+    float* dst = V + (long long)c * geo.Tp + t;
+    if (!tile_ok || c >= geo.C) {
 #pragma unroll
-      for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
-      if (geo.tf32 == 2) {
-        const float hi = round_tf32(acc);
-        dst[0] = hi;
-        dst[lo_off] = round_tf32(acc - hi);
-      } else {
-        dst[0] = geo.tf32 ? round_tf32(acc) : acc;
+      for (int p = 0; p < N * N; p++) {
+        dst[(long long)p * plane] = 0.0f;
+        if (geo.tf32 == 2) dst[lo_off + (long long)p * plane] = 0.0f;
       }
-      dst += plane;
+      continue;
     }
+    const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W + off0;
+    float d[N][N];
+#pragma unroll
+    for (int a = 0; a < N; a++)
+#pragma unroll
+      for (int b = 0; b < N; b++)
+        d[a][b] = ((rowm >> a) & (colm >> b) & 1u) ? __ldg(xc + (long long)a * geo.W + b) : 0.0f;
+    // T2[i][q] = Σ_j Bᵀ[i][j] d[j][q]
+    float t2[N][N];
+#pragma unroll
+    for (int q = 0; q < N; q++)
+#pragma unroll
+      for (int i = 0; i < N; i++) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < N; j++) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
+        t2[i][q] = acc;
+      }
+    // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]; positions p = i N + l stored in ascending order
+#pragma unroll
+    for (int i = 0; i < N; i++)
+#pragma unroll
+      for (int l = 0; l < N; l++) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
+        if (geo.tf32 == 2) {
+          const float hi = round_tf32(acc);
+          dst[0] = hi;
+          dst[lo_off] = round_tf32(acc - hi);
+        } else {
+          dst[0] = geo.tf32 ? round_tf32(acc) : acc;
+        }
+        dst += plane;
+      }
+  }
 }
 
 // ------------------------------------------------------------------ K3
@@ -638,7 +661,8 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   }
   if (forked) cudaEventRecord(side.join, fs);
   {
-    const long long tot = (long long)g.Cp * g.Tp;
+    const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
+    const long long tot = (long long)(g.Cp / cpt) * g.Tp;
     const auto ik = cfg->ik;
     timed_launch("layer_input", stream, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt); });
     launches++;
