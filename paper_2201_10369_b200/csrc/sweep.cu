@@ -292,7 +292,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   double* partial = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.partial);
   double* ref_part = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_part);
   double* ref_tot = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_tot);
-  const size_t smem = huff    ? (size_t)(2 * n - 1) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
+  const size_t smem = huff    ? (size_t)huff_slot_columns(dims, n) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
                                     (size_t)kMaxCpc * 4 * kPartial * 8
                       : mixed ? (size_t)dy * kSwThreads * 8 + (size_t)kMaxCpc * 4 * kPartial * 8
                               : smem_bytes(dims, m, r, lay);

@@ -28,6 +28,8 @@ __host__ __device__ constexpr int huff_prog_bytes(int m, int r) {
 }
 __host__ __device__ constexpr int huff_prog_words(int m, int r) { return (huff_prog_bytes(m, r) + 3) / 4; }
 constexpr unsigned char kHuffNone = 255;
+// per-thread slot columns: one dot at a time in 1D, N dots sharing a program in 2D
+__host__ __device__ constexpr int huff_slot_columns(int dims, int n) { return dims == 1 ? 2 * n - 1 : n * (2 * n - 1); }
 
 __device__ __forceinline__ u64 hmul2(u64 a, float c) {
   u64 d, cc;
@@ -65,7 +67,34 @@ __device__ __forceinline__ u64 huff_dot(const float* coef, int cs, const u64 (&x
   return res == kHuffNone ? 0ull : slot[res * kSwThreads];
 }
 
-// smem: slots [2N-1][kSwThreads] u64, y64 [MM][2][kSwThreads] double, sacc
+// ND dot products sharing one row program: Σ_j coef[j] * x[d][j] for d < ND.  Each dot has
+// its own slot column (slot + d * (2 LEN - 1) * kSwThreads), so the ND addition chains are
+// independent (ILP) and the program decode is paid once.
+template <int LEN, int ND>
+__device__ __forceinline__ void huff_dot_multi(const float* coef, const u64 (&x)[ND][LEN], const unsigned char* rec,
+                                               u64* slot, u64 (&out)[ND]) {
+  constexpr int S = (2 * LEN - 1) * kSwThreads;   // slot column stride per dot
+#pragma unroll
+  for (int j = 0; j < LEN; j++) {
+    const float c = coef[j];
+#pragma unroll
+    for (int d = 0; d < ND; d++) slot[d * S + j * kSwThreads] = hmul2(x[d][j], c);
+  }
+  const int nops = rec[0];
+#pragma unroll
+  for (int k = 0; k < LEN - 1; k++) {
+    if (k < nops) {
+      const int a = rec[2 + 2 * k] * kSwThreads, b = rec[3 + 2 * k] * kSwThreads;
+#pragma unroll
+      for (int d = 0; d < ND; d++) slot[d * S + (LEN + k) * kSwThreads] = hadd2(slot[d * S + a], slot[d * S + b]);
+    }
+  }
+  const int res = rec[1];
+#pragma unroll
+  for (int d = 0; d < ND; d++) out[d] = res == kHuffNone ? 0ull : slot[d * S + res * kSwThreads];
+}
+
+// smem: slots [huff_slot_columns][kSwThreads] u64, y64 [MM][2][kSwThreads] double, sacc
 template <int DIMS, int M, int R, bool DUMP>
 __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                                 const __grid_constant__ IdxParam DI) {
@@ -76,8 +105,9 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
   constexpr int TPB = kSwThreads * 2;
   constexpr int RG = huff_rec_bytes(R), RB = huff_rec_bytes(N);
   extern __shared__ __align__(16) unsigned char smem[];
-  u64* slots = reinterpret_cast<u64*>(smem);                        // [2N-1][kSwThreads]
-  double* sy = reinterpret_cast<double*>(slots + (2 * N - 1) * kSwThreads);   // [DY][2][kSwThreads]
+  constexpr int SLOTS = huff_slot_columns(DIMS, N);
+  u64* slots = reinterpret_cast<u64*>(smem);                        // [SLOTS][kSwThreads]
+  double* sy = reinterpret_cast<double*>(slots + SLOTS * kSwThreads);   // [DY][2][kSwThreads]
   double* sacc = sy + DY * 2 * kSwThreads;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   u64* slot = slots + tid;
@@ -139,48 +169,61 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
 #pragma unroll
           for (int p = 0; p < M; p++) y[p] = huff_dot<N>(AT + p * N, 1, mw, pa + p * RB, slot);
         } else {
+          // Every pass evaluates the dots that share a row program together (huff_dot_multi).
           // U = G g Gᵀ: T1[i][q] = dot(G row i, g[.][q]); U[i][l] = dot(G row l, T1[i][.])
+          u64 T1[N][R];
+#pragma unroll
+          for (int i = 0; i < N; i++) {
+            u64 cols[R][R];
+#pragma unroll
+            for (int q = 0; q < R; q++)
+#pragma unroll
+              for (int j = 0; j < R; j++) cols[q][j] = g[j * R + q];
+            huff_dot_multi<R, R>(G + i * R, cols, pg + i * RG, slot, T1[i]);
+          }
           u64 U[N][N];
 #pragma unroll
-          for (int i = 0; i < N; i++) {
-            u64 t1[R];
+          for (int l = 0; l < N; l++) {
+            u64 o[N];
+            huff_dot_multi<R, N>(G + l * R, T1, pg + l * RG, slot, o);
 #pragma unroll
-            for (int q = 0; q < R; q++) {
-              u64 col[R];
-#pragma unroll
-              for (int j = 0; j < R; j++) col[j] = g[j * R + q];
-              t1[q] = huff_dot<R>(G + i * R, 1, col, pg + i * RG, slot);
-            }
-#pragma unroll
-            for (int l = 0; l < N; l++) U[i][l] = huff_dot<R>(G + l * R, 1, t1, pg + l * RG, slot);
+            for (int i = 0; i < N; i++) U[i][l] = o[i];
           }
-          // V = Bᵀ d B row by row, Mw = U ⊙ V (kept in U)
+          // T2[i][q] = dot(Bᵀ row i, d[.][q]); V[i][l] = dot(Bᵀ row l, T2[i][.]); Mw = U ⊙ V
+          u64 T2[N][N];
 #pragma unroll
           for (int i = 0; i < N; i++) {
-            u64 t2[N];
+            u64 cols[N][N];
 #pragma unroll
-            for (int q = 0; q < N; q++) {
-              u64 col[N];
+            for (int q = 0; q < N; q++)
 #pragma unroll
-              for (int j = 0; j < N; j++) col[j] = d[j * N + q];
-              t2[q] = huff_dot<N>(BT + i * N, 1, col, pb + i * RB, slot);
-            }
-#pragma unroll
-            for (int l = 0; l < N; l++) U[i][l] = hmulv2(U[i][l], huff_dot<N>(BT + l * N, 1, t2, pb + l * RB, slot));
+              for (int j = 0; j < N; j++) cols[q][j] = d[j * N + q];
+            huff_dot_multi<N, N>(BT + i * N, cols, pb + i * RB, slot, T2[i]);
           }
-          // Y = Aᵀ Mw A: T3[p][l] = dot(Aᵀ row p, Mw[.][l]); Y[p][s] = dot(Aᵀ row s, T3[p][.])
+#pragma unroll
+          for (int l = 0; l < N; l++) {
+            u64 o[N];
+            huff_dot_multi<N, N>(BT + l * N, T2, pb + l * RB, slot, o);
+#pragma unroll
+            for (int i = 0; i < N; i++) U[i][l] = hmulv2(U[i][l], o[i]);
+          }
+          // T3[p][l] = dot(Aᵀ row p, Mw[.][l]); Y[p][q] = dot(Aᵀ row q, T3[p][.])
+          u64 T3[M][N];
 #pragma unroll
           for (int p = 0; p < M; p++) {
-            u64 t3[N];
+            u64 cols[N][N];
 #pragma unroll
-            for (int l = 0; l < N; l++) {
-              u64 col[N];
+            for (int l = 0; l < N; l++)
 #pragma unroll
-              for (int i = 0; i < N; i++) col[i] = U[i][l];
-              t3[l] = huff_dot<N>(AT + p * N, 1, col, pa + p * RB, slot);
-            }
+              for (int i = 0; i < N; i++) cols[l][i] = U[i][l];
+            huff_dot_multi<N, N>(AT + p * N, cols, pa + p * RB, slot, T3[p]);
+          }
 #pragma unroll
-            for (int q = 0; q < M; q++) y[p * M + q] = huff_dot<N>(AT + q * N, 1, t3, pa + q * RB, slot);
+          for (int q = 0; q < M; q++) {
+            u64 o[M];
+            huff_dot_multi<N, M>(AT + q * N, T3, pa + q * RB, slot, o);
+#pragma unroll
+            for (int p = 0; p < M; p++) y[p * M + q] = o[p];
           }
         }
         if (DUMP) {
