@@ -216,6 +216,27 @@ struct Stat32 {
     r1 = v1;
     rm = vm;
   }
+  // cheaper variant (1D kernel, where the reduction is amortised over fewer tiles): max|e|
+  // >= 0 orders like its bit pattern -> one redux.sync.max.u32; the two sums share one
+  // butterfly (after the xor-16 exchange lanes < 16 carry Σ|e| and lanes >= 16 Σe²).
+  // Results valid in lane 0.
+  __device__ __forceinline__ void warp_reduce_lane0(double& r0, double& r1, double& rm) const {
+    float a, b;
+    split(s0, a, b);
+    const float v0 = a + b;
+    split(s1, a, b);
+    const float v1 = a + b;
+    split(m0, a, b);
+    const unsigned vm = __float_as_uint(fmaxf(a, b));
+    const bool upper = (threadIdx.x & 16) != 0;
+    float v = upper ? v1 : v0;
+    v += __shfl_xor_sync(0xffffffffu, upper ? v0 : v1, 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    r0 = v;
+    r1 = __shfl_sync(0xffffffffu, v, 16);
+    rm = __uint_as_float(__reduce_max_sync(0xffffffffu, vm));
+  }
 };
 
 // ------------------------------------------------------------------ K6: fp64 references
@@ -852,7 +873,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
           rm = st.m0[0];
           rn = (double)st.nonfin;
         } else {
-          st32.warp_reduce(r0, r1, rm);
+          st32.warp_reduce_lane0(r0, r1, rm);
         }
         if (lane == 0) {
           double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
