@@ -358,63 +358,103 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
 
 // ------------------------------------------------------------------ K5 scoring
 // fp64 direct valid correlation of the same fp32 x, w (eq:conv P:112, O7), compared with
-// the Winograd output y.  CTA = (image, 16 output channels, 16 x 16 outputs):
+// the Winograd output y.  CTA = (image, 16 output channels, 32 x 16 outputs):
 // per input channel the x patch (converted to fp64) and the 16 filters are staged in
-// shared memory; each thread accumulates 16 outputs (one position, 16 channels) with DFMA
+// shared memory; each thread accumulates 32 outputs (two positions, 16 channels) with DFMA
 // in the oracle's order (Σ_c Σ_u Σ_v ascending).  Statistics: warp butterflies, then a
 // fixed-order combination of the 8 warps -> one partial per CTA (deterministic).
-constexpr int kScT = 16;   // outputs per CTA side
+constexpr int kScW = 16;   // output columns per CTA
+constexpr int kScH = 32;   // output rows per CTA (each thread: rows ty and ty + 16)
 constexpr int kScK = 16;   // output channels per CTA
 
 template <int R>
-__global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
+__global__ void __launch_bounds__(256, 2) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
                                                     const float* __restrict__ y, Geo geo,
                                                     double* __restrict__ partial) {
-  constexpr int P = kScT + R - 1;
-  __shared__ double sx[P * P];
-  __shared__ __align__(16) double sw[R * R][kScK];
+  constexpr int PH = kScH + R - 1, PW = kScW + R - 1;
+  constexpr int XPT = (PH * PW + 255) / 256, WPT = (kScK * R * R + 255) / 256;   // staged values per thread
+  __shared__ double sx[2][PH * PW];
+  __shared__ __align__(16) double sw[2][R * R][kScK];
   __shared__ double red[8][7];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int tiles_w = (geo.Wo + kScT - 1) / kScT;
-  const int h0 = (blockIdx.x / tiles_w) * kScT, w0 = (blockIdx.x % tiles_w) * kScT;
+  const int tiles_w = (geo.Wo + kScW - 1) / kScW;
+  const int h0 = (blockIdx.x / tiles_w) * kScH, w0 = (blockIdx.x % tiles_w) * kScW;
   const int k0 = blockIdx.y * kScK, img = blockIdx.z;
-  double acc[kScK];
-#pragma unroll
-  for (int k = 0; k < kScK; k++) acc[k] = 0.0;
-  for (int c = 0; c < geo.C; c++) {
-    __syncthreads();
+  // channel c + 1 is fetched into registers while channel c is accumulated (double-buffered
+  // shared memory, one barrier per channel); each thread owns two output rows, so every
+  // weight read from shared memory feeds two DFMAs
+  float xr[XPT], wr[WPT];
+  auto fetch = [&](int c) {
     const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
-    for (int idx = tid; idx < P * P; idx += 256) {
-      const int a = idx / P, b = idx - (idx / P) * P;
+#pragma unroll
+    for (int q = 0; q < XPT; q++) {
+      const int idx = tid + q * 256;
+      const int a = idx / PW, b = idx - (idx / PW) * PW;
       const int hh = h0 - geo.pad + a, wx = w0 - geo.pad + b;
-      sx[idx] = (hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W) ? (double)__ldg(xc + (long long)hh * geo.W + wx)
-                                                                 : 0.0;
+      xr[q] = (idx < PH * PW && hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W)
+                  ? __ldg(xc + (long long)hh * geo.W + wx)
+                  : 0.0f;
     }
-    for (int idx = tid; idx < kScK * R * R; idx += 256) {
+#pragma unroll
+    for (int q = 0; q < WPT; q++) {
+      const int idx = tid + q * 256;
       const int kk = idx / (R * R), e = idx - kk * (R * R);
-      sw[e][kk] = (k0 + kk < geo.K) ? (double)__ldg(w + ((long long)(k0 + kk) * geo.C + c) * R * R + e) : 0.0;
+      wr[q] = (idx < kScK * R * R && k0 + kk < geo.K) ? __ldg(w + ((long long)(k0 + kk) * geo.C + c) * R * R + e) : 0.0f;
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < XPT; q++) {
+      const int idx = tid + q * 256;
+      if (idx < PH * PW) sx[buf][idx] = (double)xr[q];
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; q++) {
+      const int idx = tid + q * 256;
+      if (idx < kScK * R * R) sw[buf][idx % (R * R)][idx / (R * R)] = (double)wr[q];
+    }
+  };
+  double acc[2][kScK];
+#pragma unroll
+  for (int j = 0; j < 2; j++)
+#pragma unroll
+    for (int k = 0; k < kScK; k++) acc[j][k] = 0.0;
+  if (geo.C > 0) {
+    fetch(0);
+    store(0);
+  }
+  __syncthreads();
+  for (int c = 0; c < geo.C; c++) {
+    const int buf = c & 1;
+    if (c + 1 < geo.C) fetch(c + 1);
 #pragma unroll
     for (int u = 0; u < R; u++)
 #pragma unroll
       for (int v = 0; v < R; v++) {
-        const double xv = sx[(ty + u) * P + tx + v];
+        const double xa = sx[buf][(ty + u) * PW + tx + v];
+        const double xb = sx[buf][(ty + 16 + u) * PW + tx + v];
 #pragma unroll
         for (int k2 = 0; k2 < kScK / 2; k2++) {
-          const double2 wv = *reinterpret_cast<const double2*>(&sw[u * R + v][2 * k2]);
-          acc[2 * k2] = __fma_rn(wv.x, xv, acc[2 * k2]);
-          acc[2 * k2 + 1] = __fma_rn(wv.y, xv, acc[2 * k2 + 1]);
+          const double2 wv = *reinterpret_cast<const double2*>(&sw[buf][u * R + v][2 * k2]);
+          acc[0][2 * k2] = __fma_rn(wv.x, xa, acc[0][2 * k2]);
+          acc[0][2 * k2 + 1] = __fma_rn(wv.y, xa, acc[0][2 * k2 + 1]);
+          acc[1][2 * k2] = __fma_rn(wv.x, xb, acc[1][2 * k2]);
+          acc[1][2 * k2 + 1] = __fma_rn(wv.y, xb, acc[1][2 * k2 + 1]);
         }
       }
+    if (c + 1 < geo.C) store(buf ^ 1);
+    __syncthreads();
   }
   double s0 = 0, s1 = 0, s2 = 0, m0 = 0, m1 = 0, n = 0, nf = 0;
-  const int h = h0 + ty, ww = w0 + tx;
-  if (h < geo.Ho && ww < geo.Wo) {
+  const int ww = w0 + tx;
+#pragma unroll
+  for (int j = 0; j < 2; j++) {
+    const int h = h0 + ty + 16 * j;
+    if (h >= geo.Ho || ww >= geo.Wo) continue;
 #pragma unroll
     for (int k = 0; k < kScK; k++) {
       if (k0 + k >= geo.K) break;
-      const double r = acc[k];
+      const double r = acc[j][k];
       const double e = (double)y[(((long long)img * geo.K + k0 + k) * geo.Ho + h) * geo.Wo + ww] - r;
       s2 += fabs(r);
       m1 = fmax(m1, fabs(r));
@@ -531,7 +571,7 @@ LayerCfg make_layer_cfg() {
 }
 
 dim3 score_grid(const Geo& g) {
-  return dim3((unsigned)(((g.Ho + kScT - 1) / kScT) * ((g.Wo + kScT - 1) / kScT)), (unsigned)((g.K + kScK - 1) / kScK),
+  return dim3((unsigned)(((g.Ho + kScH - 1) / kScH) * ((g.Wo + kScW - 1) / kScW)), (unsigned)((g.K + kScK - 1) / kScK),
               (unsigned)g.N);
 }
 
