@@ -105,7 +105,11 @@ int wino_points_to_matrices(int m, int r, const double* points, int n,
  * Arithmetic (the parity semantics, DESIGN.md §2.3 "F32-FMA"): each dot product is an
  * ascending fmaf chain from +0; 2D transforms left product first; the channel sum is one
  * ascending-c fmaf chain per (k, tile, Winograd position), no split, no TF32.
- * Output is bit-identical to the oracle's O5 layer.  Asynchronous on `stream`. */
+ * Output is bit-identical to the oracle's O5 layer.  Asynchronous on `stream`; the filter
+ * transform runs on a library-owned side stream (one per host thread and device) forked
+ * from and joined back to `stream` with events, so the call stays stream-ordered and
+ * graph-capturable.  wino_conv2d_workspace_bytes() is large enough for every variant of
+ * (2c) as well. */
 size_t wino_conv2d_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m);
 int wino_conv2d_fp32(const float* x, const float* w, float* y,
                      int N, int C, int H, int W, int K, int r, int pad, int m,
@@ -164,7 +168,7 @@ int wino_last_launch_count(void);
 
 /* Kernel timing hook (profiling / bench.py roofline).  While enabled, every launch is
  * bracketed by two cudaEvents recorded on its own stream and filed under its kernel
- * family: "sweep1d", "sweep2d", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
+ * family: "sweep1d", "sweep2d", "sweep_huffman", "sweep_mixed", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
  * "layer_filter", "layer_input", "layer_gemm", "layer_gemm_tf32", "layer_gemm_3xtf32", "layer_output", "layer_score",
  * "layer_score_finalize", "relu_pool".  wino_timing_read() synchronises on the recorded events and
  * returns the summed milliseconds and launch count of one family since the last reset.
