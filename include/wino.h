@@ -105,7 +105,9 @@ int wino_points_to_matrices(int m, int r, const double* points, int n,
  * Arithmetic (the parity semantics, DESIGN.md §2.3 "F32-FMA"): each dot product is an
  * ascending fmaf chain from +0; 2D transforms left product first; the channel sum is one
  * ascending-c fmaf chain per (k, tile, Winograd position), no split, no TF32.
- * Output is bit-identical to the oracle's O5 layer.  Asynchronous on `stream`; the filter
+ * Output is bit-identical to the oracle's O5 layer.  N == 0 or K == 0 (empty output) is a
+ * successful no-op (nothing enqueued, statistics untouched); C, H, W >= 1 are required.
+ * Asynchronous on `stream`; the filter
  * transform runs on a library-owned side stream (one per host thread and device) forked
  * from and joined back to `stream` with events, so the call stays stream-ordered and
  * graph-capturable.  wino_conv2d_workspace_bytes() is large enough for every variant of

@@ -157,8 +157,8 @@ int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, 
                         double* d_maxs, unsigned flags, void* stream) {
   reset_launches();
   if (!x || !w || !y || !points) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
-  if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || r < 1 || m < 1 || pad < 0)
-    return set_error(WINO_E_INVALID_ARG, "non-positive size or negative pad");
+  if (N < 0 || C < 1 || H < 1 || W < 1 || K < 0 || r < 1 || m < 1 || pad < 0)
+    return set_error(WINO_E_INVALID_ARG, "negative batch / output channels, non-positive size or negative pad");
   if (flags & ~(WINO_CONV_TF32 | WINO_CONV_3XTF32)) return set_error(WINO_E_INVALID_ARG, "unknown flags");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
@@ -169,6 +169,7 @@ int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, 
   std::vector<double> AT(m * n), G(n * r), BT(n * n);
   const int s = build_r64(m, r, points, n, AT.data(), G.data(), BT.data());
   if (s != WINO_OK) return set_error(s, "points: %s", build_error_detail(s));
+  if (N == 0 || K == 0) return finish(WINO_OK);   // empty batch / no filters: nothing to enqueue
   std::vector<float> ATf(m * n), Gf(n * r), BTf(n * n);
   to_f32(AT.data(), m * n, ATf.data());
   to_f32(G.data(), n * r, Gf.data());

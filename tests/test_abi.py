@@ -127,3 +127,27 @@ def test_workspace_sizes():
     b = api.wino_conv2d_workspace_bytes(32, 256, 56, 56, 256, 3, 1, 6)
     assert b > 3 * 64 * 256 * 3200 * 4 // 2
     assert api.wino_conv2d_workspace_bytes(1, 1, 1, 1, 1, 3, 0, 2) == 0
+
+
+def test_layer_empty_batch_and_validation_without_device():
+    """Host-side paths of wino_conv2d_fp32 that enqueue nothing: N == 0 / K == 0 are
+    successful no-ops (dummy, never dereferenced pointers); validation errors are reported
+    before any device call."""
+    import ctypes
+    L = _lib.load()
+    buf = (ctypes.c_float * 16)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    pts = np.array(OP.f23_c(1.0), dtype=np.float64)
+    pp = pts.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    for N, K in ((0, 8), (2, 0)):
+        st = L.wino_conv2d_fp32(p, p, p, N, 8, 16, 16, K, 3, 1, 2, pp, None, 0, None, None, None)
+        assert st == 0, st
+        assert L.wino_last_launch_count() == 0
+    st = L.wino_conv2d_fp32(p, p, p, -1, 8, 16, 16, 8, 3, 1, 2, pp, None, 0, None, None, None)
+    assert st == 1
+    bad = np.array([0.0, 0.0, 1.0, INF])
+    st = L.wino_conv2d_fp32(p, p, p, 0, 8, 16, 16, 8, 3, 1, 2, bad.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                            None, 0, None, None, None)
+    assert st == 3                                   # point validation still applies
+    st = L.wino_conv2d_fp32_ex(p, p, p, 0, 8, 16, 16, 8, 3, 1, 2, pp, None, 0, None, None, 8, None)
+    assert st == 1                                   # unknown flag
