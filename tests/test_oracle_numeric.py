@@ -405,3 +405,40 @@ def test_huffman_curve_minimum_region(dims, lo, hi):
     i = int(np.argmin(e))
     assert lo <= cs[i] <= hi, cs[i]
     assert e[0] >= 1.25 * e[i] and e[-1] >= 1.25 * e[i]
+
+
+def _fixture_points(finite):
+    pts = []
+    for v in finite:
+        if isinstance(v, str):
+            sign = -1.0 if v.startswith("-") else 1.0
+            pts.append(sign * (1.0 / float(v.lstrip("-").split("/")[1])))
+        else:
+            pts.append(float(v))
+    return sorted(pts) + [INF]
+
+
+T78 = json.load(open(os.path.join(GOLD, "paper_tables_t7_t8.json")))["rows"]
+
+
+@pytest.mark.parametrize("row", T78, ids=[f"{r['dims']}d-n{r['n']}-{r['kind']}" for r in T78])
+def test_huffman_reproduces_paper_tables(row):
+    """Every T7/T8 row, kernel size 3, n = 4..10: the Huffman-mode oracle
+    (R21, the paper's order) lands within [-4 %, +9 %] of the printed error (the
+    paper averages 5000 inputs; we use 100k 1D / 20k 2D uniform[-1,1] tiles, R9).  Rows the
+    fixture marks "not reproduced" (a printed set that evaluates far from its value in every
+    summation order) are asserted to stay far, so a change of reading shows up.  The
+    1D n=4 P4 row sits at +14.5 % in every order (F(2,3) has too few terms for the order to
+    matter) and is held to +20 %."""
+    dims, n = row["dims"], row["n"]
+    pts = _fixture_points(row["finite_points"])
+    assert len(pts) == n
+    d, g = synth.random_tiles(100_000 if dims == 1 else 20_000, dims, n, 3, "uniform", seed=0)
+    s, _, _ = ref.sweep(dims, n - 2, 3, [pts], d, g, huffman=True)
+    rel = s[0, 0] / s[0, 3] / row["value"] - 1
+    if "not reproduced" in row.get("note", ""):
+        assert rel > 0.3
+    elif dims == 1 and n == 4 and row["kind"] == "prior":
+        assert -0.04 <= rel <= 0.20
+    else:
+        assert -0.04 <= rel <= 0.09, rel
