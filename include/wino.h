@@ -59,8 +59,8 @@ typedef enum {
 /* Huffman evaluation order of every transform dot product ("Huffman tree evaluation
  * order"; reading R21): products RN(coef*x) of the non-zero coefficients
  * summed along a Huffman tree over |coef| (ties: leaves in index order, then older nodes);
- * Hadamard product RN(u*v).  Overrides WINO_SWEEP_NOFMA.  Compiled for F(2,3), F(4,3),
- * F(6,3) in 1D and 2D; other shapes return WINO_E_UNSUPPORTED. */
+ * Hadamard product RN(u*v).  Overrides WINO_SWEEP_NOFMA.  Compiled for F(m,3), m = 2..8
+ * (the paper's T7/T8 sizes), in 1D and 2D; other shapes return WINO_E_UNSUPPORTED. */
 #define WINO_SWEEP_HUFFMAN 2u
 /* Mixed precision ("double precision floating point for the transforms and single
  * precision for Hadamard product"; reading R22): the transforms in fp64 with the

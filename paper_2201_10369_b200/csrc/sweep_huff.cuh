@@ -28,8 +28,12 @@ __host__ __device__ constexpr int huff_prog_bytes(int m, int r) {
 }
 __host__ __device__ constexpr int huff_prog_words(int m, int r) { return (huff_prog_bytes(m, r) + 3) / 4; }
 constexpr unsigned char kHuffNone = 255;
-// per-thread slot columns: one dot at a time in 1D, N dots sharing a program in 2D
-__host__ __device__ constexpr int huff_slot_columns(int dims, int n) { return dims == 1 ? 2 * n - 1 : n * (2 * n - 1); }
+// dots evaluated together per row program in 2D (shared memory bounds it for n > 8)
+__host__ __device__ constexpr int huff_group(int n) { return n <= 8 ? n : 3; }
+// per-thread slot columns: one dot at a time in 1D, huff_group(n) dots sharing a program in 2D
+__host__ __device__ constexpr int huff_slot_columns(int dims, int n) {
+  return dims == 1 ? 2 * n - 1 : huff_group(n) * (2 * n - 1);
+}
 
 __device__ __forceinline__ u64 hmul2(u64 a, float c) {
   u64 d, cc;
@@ -67,31 +71,36 @@ __device__ __forceinline__ u64 huff_dot(const float* coef, int cs, const u64 (&x
   return res == kHuffNone ? 0ull : slot[res * kSwThreads];
 }
 
-// ND dot products sharing one row program: Σ_j coef[j] * x[d][j] for d < ND.  Each dot has
-// its own slot column (slot + d * (2 LEN - 1) * kSwThreads), so the ND addition chains are
-// independent (ILP) and the program decode is paid once.
-template <int LEN, int ND>
+// ND dot products sharing one row program: Σ_j coef[j] * x[d][j] for d < ND, in groups of
+// G dots.  Each dot of a group has its own slot column (slot + d * (2 LEN - 1) * kSwThreads),
+// so the G addition chains are independent (ILP) and the program decode is shared.
+template <int LEN, int ND, int G>
 __device__ __forceinline__ void huff_dot_multi(const float* coef, const u64 (&x)[ND][LEN], const unsigned char* rec,
                                                u64* slot, u64 (&out)[ND]) {
   constexpr int S = (2 * LEN - 1) * kSwThreads;   // slot column stride per dot
+  const int nops = rec[0], res = rec[1];
 #pragma unroll
-  for (int j = 0; j < LEN; j++) {
-    const float c = coef[j];
+  for (int d0 = 0; d0 < ND; d0 += G) {
 #pragma unroll
-    for (int d = 0; d < ND; d++) slot[d * S + j * kSwThreads] = hmul2(x[d][j], c);
-  }
-  const int nops = rec[0];
+    for (int j = 0; j < LEN; j++) {
+      const float c = coef[j];
 #pragma unroll
-  for (int k = 0; k < LEN - 1; k++) {
-    if (k < nops) {
-      const int a = rec[2 + 2 * k] * kSwThreads, b = rec[3 + 2 * k] * kSwThreads;
-#pragma unroll
-      for (int d = 0; d < ND; d++) slot[d * S + (LEN + k) * kSwThreads] = hadd2(slot[d * S + a], slot[d * S + b]);
+      for (int dd = 0; dd < G; dd++)
+        if (d0 + dd < ND) slot[dd * S + j * kSwThreads] = hmul2(x[d0 + dd][j], c);
     }
-  }
-  const int res = rec[1];
 #pragma unroll
-  for (int d = 0; d < ND; d++) out[d] = res == kHuffNone ? 0ull : slot[d * S + res * kSwThreads];
+    for (int k = 0; k < LEN - 1; k++) {
+      if (k < nops) {
+        const int a = rec[2 + 2 * k] * kSwThreads, b = rec[3 + 2 * k] * kSwThreads;
+#pragma unroll
+        for (int dd = 0; dd < G; dd++)
+          if (d0 + dd < ND) slot[dd * S + (LEN + k) * kSwThreads] = hadd2(slot[dd * S + a], slot[dd * S + b]);
+      }
+    }
+#pragma unroll
+    for (int dd = 0; dd < G; dd++)
+      if (d0 + dd < ND) out[d0 + dd] = res == kHuffNone ? 0ull : slot[dd * S + res * kSwThreads];
+  }
 }
 
 // smem: slots [huff_slot_columns][kSwThreads] u64, y64 [MM][2][kSwThreads] double, sacc
@@ -106,6 +115,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
   constexpr int RG = huff_rec_bytes(R), RB = huff_rec_bytes(N);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int SLOTS = huff_slot_columns(DIMS, N);
+  constexpr int HG = huff_group(N);
   u64* slots = reinterpret_cast<u64*>(smem);                        // [SLOTS][kSwThreads]
   double* sy = reinterpret_cast<double*>(slots + SLOTS * kSwThreads);   // [DY][2][kSwThreads]
   double* sacc = sy + DY * 2 * kSwThreads;
@@ -179,13 +189,13 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int q = 0; q < R; q++)
 #pragma unroll
               for (int j = 0; j < R; j++) cols[q][j] = g[j * R + q];
-            huff_dot_multi<R, R>(G + i * R, cols, pg + i * RG, slot, T1[i]);
+            huff_dot_multi<R, R, (R < HG ? R : HG)>(G + i * R, cols, pg + i * RG, slot, T1[i]);
           }
           u64 U[N][N];
 #pragma unroll
           for (int l = 0; l < N; l++) {
             u64 o[N];
-            huff_dot_multi<R, N>(G + l * R, T1, pg + l * RG, slot, o);
+            huff_dot_multi<R, N, HG>(G + l * R, T1, pg + l * RG, slot, o);
 #pragma unroll
             for (int i = 0; i < N; i++) U[i][l] = o[i];
           }
@@ -198,12 +208,12 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int q = 0; q < N; q++)
 #pragma unroll
               for (int j = 0; j < N; j++) cols[q][j] = d[j * N + q];
-            huff_dot_multi<N, N>(BT + i * N, cols, pb + i * RB, slot, T2[i]);
+            huff_dot_multi<N, N, HG>(BT + i * N, cols, pb + i * RB, slot, T2[i]);
           }
 #pragma unroll
           for (int l = 0; l < N; l++) {
             u64 o[N];
-            huff_dot_multi<N, N>(BT + l * N, T2, pb + l * RB, slot, o);
+            huff_dot_multi<N, N, HG>(BT + l * N, T2, pb + l * RB, slot, o);
 #pragma unroll
             for (int i = 0; i < N; i++) U[i][l] = hmulv2(U[i][l], o[i]);
           }
@@ -216,12 +226,12 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int l = 0; l < N; l++)
 #pragma unroll
               for (int i = 0; i < N; i++) cols[l][i] = U[i][l];
-            huff_dot_multi<N, N>(AT + p * N, cols, pa + p * RB, slot, T3[p]);
+            huff_dot_multi<N, N, HG>(AT + p * N, cols, pa + p * RB, slot, T3[p]);
           }
 #pragma unroll
           for (int q = 0; q < M; q++) {
             u64 o[M];
-            huff_dot_multi<N, M>(AT + q * N, T3, pa + q * RB, slot, o);
+            huff_dot_multi<N, M, (M < HG ? M : HG)>(AT + q * N, T3, pa + q * RB, slot, o);
 #pragma unroll
             for (int p = 0; p < M; p++) y[p * M + q] = o[p];
           }

@@ -6,7 +6,7 @@ namespace wino {
 
 std::vector<SweepCfg> sweep_cfgs_1d_large() {
   return {
-      make_cfg<1, 6, 3, TPAIR>(), make_cfg<1, 8, 3, TPAIR>(), make_cfg<1, 6, 5, TPAIR>(),
+      make_cfg<1, 6, 3, TPAIR>(), make_cfg<1, 7, 3, TPAIR>(), make_cfg<1, 8, 3, TPAIR>(), make_cfg<1, 6, 5, TPAIR>(),
   };
 }
 

@@ -98,3 +98,55 @@ def test_huffman_unsupported_shape():
     with pytest.raises(_lib.WinoError) as ei:
         _stats(2, 4, 5, [OP.n8_c1c2(1.5, 3.1)], d, g)
     assert ei.value.status == 8
+
+
+def _fixture_rows():
+    import json, os
+    rows = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_tables_t7_t8.json")))["rows"]
+    return rows
+
+
+def _pts(finite):
+    out = []
+    for v in finite:
+        if isinstance(v, str):
+            sign = -1.0 if v.startswith("-") else 1.0
+            out.append(sign * (1.0 / float(v.lstrip("-").split("/")[1])))
+        else:
+            out.append(float(v))
+    return sorted(out) + [INF]
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+def test_huffman_all_paper_sizes_bitexact(dims):
+    """Every T7/T8 point set (n = 4..10) through the GPU Huffman kernels: outputs
+    bit-identical to the oracle on 517 tiles."""
+    rows = [r for r in _fixture_rows() if r["dims"] == dims]
+    for n in sorted({r["n"] for r in rows}):
+        sets = [_pts(r["finite_points"]) for r in rows if r["n"] == n]
+        d, g = synth.random_tiles(517, dims, n, 3, "uniform", seed=50 + n)
+        st, y = _outputs(dims, n - 2, 3, sets, d, g)
+        assert np.all(st == 0)
+        _, _, y_ref = ref.sweep(dims, n - 2, 3, sets, d, g, huffman=True, n_dump=d.shape[0])
+        assert np.array_equal(y, y_ref), n
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+def test_huffman_paper_tables_on_gpu(dims):
+    """The paper's T7/T8 values through the C ABI at 100k tiles (the bench workload size):
+    the reproduced rows within [-4 %, +9 %] (1D n=4 P4: +20 %), the two recorded
+    non-reproducible rows far above."""
+    rows = [r for r in _fixture_rows() if r["dims"] == dims]
+    for n in sorted({r["n"] for r in rows}):
+        rs = [r for r in rows if r["n"] == n]
+        d, g = synth.random_tiles(100_000, dims, n, 3, "uniform", seed=0)
+        st, s, _ = _stats(dims, n - 2, 3, [_pts(r["finite_points"]) for r in rs], d, g)
+        assert np.all(st == 0)
+        for r, row in zip(s, rs):
+            rel = r[0] / r[3] / row["value"] - 1
+            if "not reproduced" in row.get("note", ""):
+                assert rel > 0.3
+            elif dims == 1 and n == 4 and row["kind"] == "prior":
+                assert -0.04 <= rel <= 0.20
+            else:
+                assert -0.04 <= rel <= 0.09, (n, row["kind"], rel)
