@@ -103,6 +103,21 @@ __device__ __forceinline__ void huff_dot_multi(const float* coef, const u64 (&x)
   }
 }
 
+// Out-of-line wrapper for n > 8: the fully inlined 2D kernels for F(7,3) / F(8,3) take
+// minutes to compile; calls keep the code size linear (the variant is not the hot path).
+template <int LEN, int ND, int G>
+__device__ __noinline__ void huff_dot_multi_ool(const float* coef, const u64 (&x)[ND][LEN], const unsigned char* rec,
+                                                u64* slot, u64 (&out)[ND]) {
+  huff_dot_multi<LEN, ND, G>(coef, x, rec, slot, out);
+}
+
+template <int LEN, int ND, int G, bool OOL>
+__device__ __forceinline__ void huff_dot_rows(const float* coef, const u64 (&x)[ND][LEN], const unsigned char* rec,
+                                              u64* slot, u64 (&out)[ND]) {
+  if constexpr (OOL) huff_dot_multi_ool<LEN, ND, G>(coef, x, rec, slot, out);
+  else huff_dot_multi<LEN, ND, G>(coef, x, rec, slot, out);
+}
+
 // smem: slots [huff_slot_columns][kSwThreads] u64, y64 [MM][2][kSwThreads] double, sacc
 template <int DIMS, int M, int R, bool DUMP>
 __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
@@ -189,13 +204,13 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int q = 0; q < R; q++)
 #pragma unroll
               for (int j = 0; j < R; j++) cols[q][j] = g[j * R + q];
-            huff_dot_multi<R, R, (R < HG ? R : HG)>(G + i * R, cols, pg + i * RG, slot, T1[i]);
+            huff_dot_rows<R, R, (R < HG ? R : HG), (N > 8)>(G + i * R, cols, pg + i * RG, slot, T1[i]);
           }
           u64 U[N][N];
 #pragma unroll
           for (int l = 0; l < N; l++) {
             u64 o[N];
-            huff_dot_multi<R, N, HG>(G + l * R, T1, pg + l * RG, slot, o);
+            huff_dot_rows<R, N, HG, (N > 8)>(G + l * R, T1, pg + l * RG, slot, o);
 #pragma unroll
             for (int i = 0; i < N; i++) U[i][l] = o[i];
           }
@@ -208,12 +223,12 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int q = 0; q < N; q++)
 #pragma unroll
               for (int j = 0; j < N; j++) cols[q][j] = d[j * N + q];
-            huff_dot_multi<N, N, HG>(BT + i * N, cols, pb + i * RB, slot, T2[i]);
+            huff_dot_rows<N, N, HG, (N > 8)>(BT + i * N, cols, pb + i * RB, slot, T2[i]);
           }
 #pragma unroll
           for (int l = 0; l < N; l++) {
             u64 o[N];
-            huff_dot_multi<N, N, HG>(BT + l * N, T2, pb + l * RB, slot, o);
+            huff_dot_rows<N, N, HG, (N > 8)>(BT + l * N, T2, pb + l * RB, slot, o);
 #pragma unroll
             for (int i = 0; i < N; i++) U[i][l] = hmulv2(U[i][l], o[i]);
           }
@@ -226,12 +241,12 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int l = 0; l < N; l++)
 #pragma unroll
               for (int i = 0; i < N; i++) cols[l][i] = U[i][l];
-            huff_dot_multi<N, N, HG>(AT + p * N, cols, pa + p * RB, slot, T3[p]);
+            huff_dot_rows<N, N, HG, (N > 8)>(AT + p * N, cols, pa + p * RB, slot, T3[p]);
           }
 #pragma unroll
           for (int q = 0; q < M; q++) {
             u64 o[M];
-            huff_dot_multi<N, M, (M < HG ? M : HG)>(AT + q * N, T3, pa + q * RB, slot, o);
+            huff_dot_rows<N, M, (M < HG ? M : HG), (N > 8)>(AT + q * N, T3, pa + q * RB, slot, o);
 #pragma unroll
             for (int p = 0; p < M; p++) y[p * M + q] = o[p];
           }
