@@ -526,6 +526,17 @@ def main():
                 "workload": f"configs[1] 2D {sp.spec.dist} sweep ({S} c x {T} tiles), {note}",
                 "ms": hms, "value": S * T / (hms * 1e-3), "unit": "tile-evals/s",
                 "argmin_c": float(sp.spec.params[i]) if i is not None else None, "min_mae": best}
+            if vname == "mixed_2d":
+                # dense fp64 transforms: 2D F(4x4,3x3) = 6*3*3 + 6*6*3 + 6*6*6*2 + 4*6*6 + 4*4*6 DFMA
+                dfma = 6 * 3 * 3 + 6 * 6 * 3 + 2 * 6 * 6 * 6 + 4 * 6 * 6 + 4 * 4 * 6
+                nsm_ = torch.cuda.get_device_properties(dev).multi_processor_count
+                fp64_peak = nsm_ * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+                ach = S * T * dfma * 2 / (hms * 1e-3) / 1e12
+                variants[vname]["roofline"] = {
+                    "bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                    "dfma_per_tile_eval": dfma,
+                    "peak_source": f"{nsm_} SMs x 64 DFMA/clk x 2 FLOP x sm_max_mhz (microbench: DFMA at half the "
+                                   "FFMA rate, profiles/r01_pipes_microbench.jsonl)"}
         del hws
 
     cpu = None
