@@ -710,19 +710,13 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   if (forked) cudaStreamWaitEvent(stream, side.join, 0);
   {
     if (tf32) {
-      static bool tattr[2] = {false, false};
+      // per call (cheap), so several devices / host threads in one process stay correct
       const auto kern = tf32 == 2 ? gemm_tf32_kernel<3> : gemm_tf32_kernel<1>;
       const int smem = tf32 == 2 ? tc::Cfg<3>::kSmem : tc::Cfg<1>::kSmem;
-      if (!tattr[tf32 - 1]) {
-        cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        tattr[tf32 - 1] = true;
-      }
-      static int n_sm = 0;
-      if (!n_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      }
+      cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int dev = 0, n_sm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
       const long long tiles = (long long)(n * n) * (g.Kp / tc::kM) * (g.Tp / tc::kN);
       const unsigned grid = (unsigned)std::min<long long>(tiles, n_sm);
       CUtensorMap tmU, tmV, tmUl, tmVl, tmM;
@@ -743,11 +737,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
       });
     } else {
       dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute((const void*)gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-        attr = true;
-      }
+      cudaFuncSetAttribute((const void*)gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
       timed_launch("layer_gemm", stream,
                    [&] { gemm_kernel<<<grid, 256, kGemmSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
     }
