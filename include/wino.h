@@ -129,6 +129,12 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y,
  *   accumulation, recovering ~fp32 accuracy (not bit-identical to the parity path).  Takes
  *   precedence over WINO_CONV_TF32. */
 #define WINO_CONV_3XTF32 2u
+/*   WINO_CONV_SCORE_PER_IMAGE: with d_sums / d_maxs non-NULL, the statistics are kept per
+ *   image: d_sums DEVICE double[N][WINO_SUMS], d_maxs DEVICE double[N][WINO_MAXS] (row n =
+ *   image n, accumulated).  Each image's statistics depend only on that image, so a
+ *   batch-sharded network reduces them over images in a fixed order and gets
+ *   results independent of the number of ranks.  Combinable with the other flags. */
+#define WINO_CONV_SCORE_PER_IMAGE 4u
 int wino_conv2d_fp32_ex(const float* x, const float* w, float* y,
                         int N, int C, int H, int W, int K, int r, int pad, int m,
                         const double* points, void* workspace, size_t workspace_bytes,
@@ -146,23 +152,30 @@ int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, in
  *   d_tiles: DEVICE float[n_tiles][n^dims], g_tiles: DEVICE float[n_tiles][r^dims]
  *   (row-major n x n / r x r tiles; the SAME tiles score every candidate, O9).
  *   d_sums: DEVICE double[n_cand][WINO_SUMS], d_maxs: DEVICE double[n_cand][WINO_MAXS]
- *   (ACCUMULATED).  cand_status: HOST int[n_cand] out, per-candidate wino_status of (1);
- *   a rejected candidate is skipped (its stats untouched) and does not fail the call.
+ *   (ACCUMULATED for accepted candidates).  cand_status: HOST int[n_cand] out, per-candidate
+ *   wino_status of (1); a rejected candidate does not fail the call and its statistics rows
+ *   are OVERWRITTEN with NaN (so a caller can never read a silent 0/0 mean).
  *   workspace: DEVICE, >= wino_error_sweep_workspace_bytes(...).  flags: WINO_SWEEP_*.
  * Every output of every tile is scored against the fp64 direct correlation of the tile.
- * Asynchronous on `stream` (host matrix construction happens before the launch). */
+ * A candidate whose outputs are not all finite is scored exactly per output (n_nonfinite
+ * counts the non-finite e over the real tiles).  Asynchronous on `stream` (host matrix
+ * construction happens before the launch).  n_tiles == 0: accepted rows untouched. */
 size_t wino_error_sweep_workspace_bytes(int dims, int m, int r, int n_cand, int64_t n_tiles);
 int wino_error_sweep(int dims, int m, int r, const double* point_sets, int n_cand,
                      const float* d_tiles, const float* g_tiles, int64_t n_tiles,
                      double* d_sums, double* d_maxs, int* cand_status,
                      void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
 
-/* (3b) The sweep's fp32 outputs themselves (same kernel code path as (3), scoring off):
- *   d_y: DEVICE float[n_cand][n_tiles][m^dims].  Rejected candidates' rows are untouched.
- * Used for per-element parity against the oracle. */
+/* (3b) The same sweep with the fp32 outputs written out: the PRODUCTION kernels of (3)
+ * (the output store is a run-time branch of the same code, not a separate build), used for
+ * per-element parity against the oracle.
+ *   d_y: DEVICE float[n_cand][n_tiles][m^dims]; rows of rejected candidates are untouched.
+ *   d_sums / d_maxs: as in (3), or both NULL (statistics computed in the workspace only).
+ *   workspace: DEVICE, >= wino_error_sweep_workspace_bytes(...). */
 int wino_sweep_outputs(int dims, int m, int r, const double* point_sets, int n_cand,
                        const float* d_tiles, const float* g_tiles, int64_t n_tiles,
-                       float* d_y, int* cand_status, unsigned flags, void* stream);
+                       float* d_y, double* d_sums, double* d_maxs, int* cand_status,
+                       void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
 
 /* Number of kernel launches the last successful call on this thread enqueued
  * (for bench.py's gpu_launches count). */

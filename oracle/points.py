@@ -45,6 +45,23 @@ def n10_c1c2(c1: float, c2: float) -> List[float]:
     return canonical([0.0, -q1, -c1, c1, q1, -q2, -c2, c2, q2])
 
 
+def chebyshev(n: int) -> List[float]:
+    """Chebyshev nodes for n points ("Chebyshev nodes"): the q = n - 1 roots of T_q,
+    x_k = cos((2k - 1) pi / (2q)), k = 1..q, plus the formal inf (modified algorithm).
+    Reading X24: the set is made exactly symmetric -- node q + 1 - k is the
+    negation of node k (cos(pi - t) = -cos(t)) and the middle node of an odd q is exactly 0 --
+    so the +-x cancellations of the paper's symmetric sets hold for it too."""
+    import math
+    q = n - 1
+    x = [math.cos((2 * k - 1) * math.pi / (2 * q)) for k in range(1, q + 1)]
+    for k in range(1, q + 1):
+        if 2 * k > q + 1:
+            x[k - 1] = -x[q - k]        # mirror of node q + 1 - k
+        elif 2 * k == q + 1:
+            x[k - 1] = 0.0
+    return canonical(x)
+
+
 # prior-work ("Barabasz et al.") sets of P:291, P:623-633, P:649-659 (∞ implicit)
 P4 = canonical([0.0, -1.0, 1.0])
 P8 = canonical([0.0, -1.0, 1.0, 0.5, -0.5, 2.0, -2.0])

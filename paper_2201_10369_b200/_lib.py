@@ -34,7 +34,7 @@ SIGNATURES = [
     ("wino_error_sweep", ctypes.c_int,
      [ctypes.c_int] * 3 + [_d, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _i, _vp, _sz, ctypes.c_uint, _vp]),
     ("wino_sweep_outputs", ctypes.c_int,
-     [ctypes.c_int] * 3 + [_d, ctypes.c_int, _vp, _vp, _i64, _vp, _i, ctypes.c_uint, _vp]),
+     [ctypes.c_int] * 3 + [_d, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp, _i, _vp, _sz, ctypes.c_uint, _vp]),
     ("wino_last_launch_count", ctypes.c_int, []),
     ("wino_timing_enable", ctypes.c_int, [ctypes.c_int]),
     ("wino_timing_reset", None, []),

@@ -19,6 +19,7 @@ WINO_SWEEP_HUFFMAN = 2
 WINO_SWEEP_MIXED = 4
 WINO_CONV_TF32 = 1
 WINO_CONV_3XTF32 = 2
+WINO_CONV_SCORE_PER_IMAGE = 4
 WINO_MAX_N = 16
 
 _d = ctypes.POINTER(ctypes.c_double)
@@ -73,11 +74,24 @@ def wino_conv2d_fp32(x, w, y, pad: int, m: int, points: Sequence[float], workspa
     """x [N,C,H,W], w [K,C,r,r], y [N,K,Ho,Wo] fp32 CUDA tensors; workspace uint8 CUDA
     tensor; d_sums [5] / d_maxs [2] fp64 CUDA tensors (accumulated) or None.  flags != 0
     calls wino_conv2d_fp32_ex (WINO_CONV_TF32: the tensor-core variant)."""
+    import torch
     N, C, H, W = x.shape
     K, C2, r, r2 = w.shape
     if C2 != C or r2 != r:
         raise ValueError("weight shape mismatch")
+    Ho, Wo = H + 2 * pad - r + 1, W + 2 * pad - r + 1
+    _check_tensor("x", x, torch.float32, (N, C, H, W))
+    _check_tensor("w", w, torch.float32, (K, C, r, r))
+    _check_tensor("y", y, torch.float32, (N, K, Ho, Wo))
+    if (d_sums is None) != (d_maxs is None):
+        raise ValueError("d_sums and d_maxs: both or neither")
+    if d_sums is not None:
+        rows = (N,) if flags & WINO_CONV_SCORE_PER_IMAGE else ()
+        _check_tensor("d_sums", d_sums, torch.float64, rows + (WINO_SUMS,))
+        _check_tensor("d_maxs", d_maxs, torch.float64, rows + (WINO_MAXS,))
     pts = _np64(points)
+    if pts.shape != (m + r - 1,):
+        raise ValueError(f"points: expected {m + r - 1} values, got {pts.shape}")
     args = (_ptr(x), _ptr(w), _ptr(y), N, C, H, W, K, r, pad, m, pts.ctypes.data_as(_d),
             _ptr(workspace), workspace.numel() * workspace.element_size(), _ptr(d_sums), _ptr(d_maxs))
     if flags:
@@ -90,9 +104,10 @@ def wino_conv2d_fp32(x, w, y, pad: int, m: int, points: Sequence[float], workspa
 
 def wino_relu_pool_fp32(x, y, pool: int, stream=None) -> None:
     """y = maxpool_pool(ReLU(x)); x [N,C,H,W], y [N,C,H/pool,W/pool] fp32 CUDA tensors."""
+    import torch
     N, C, H, W = x.shape
-    if tuple(y.shape) != (N, C, H // pool, W // pool):
-        raise ValueError("output shape mismatch")
+    _check_tensor("x", x, torch.float32, (N, C, H, W))
+    _check_tensor("y", y, torch.float32, (N, C, H // pool, W // pool))
     check(load().wino_relu_pool_fp32(_ptr(x), _ptr(y), N, C, H, W, pool, _stream_ptr(stream)), "wino_relu_pool_fp32")
 
 
@@ -100,31 +115,76 @@ def wino_error_sweep_workspace_bytes(dims: int, m: int, r: int, n_cand: int, n_t
     return int(load().wino_error_sweep_workspace_bytes(dims, m, r, n_cand, n_tiles))
 
 
+def _check_tensor(name, t, dtype, shape):
+    """Argument validation before a raw pointer crosses the ABI (a wrong dtype or too few
+    rows would make the kernels read or write out of bounds)."""
+    import torch
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: expected {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return torch
+
+
+def _sweep_args(dims, m, r, point_sets, d_tiles, g_tiles):
+    import torch
+    if dims not in (1, 2):
+        raise ValueError("dims must be 1 or 2")
+    n = m + r - 1
+    ps = _np64(point_sets)
+    if ps.size == 0:
+        ps = ps.reshape(0, n)
+    if ps.ndim != 2 or ps.shape[1] != n:
+        raise ValueError(f"point_sets: expected [S, {n}], got {ps.shape}")
+    S = ps.shape[0]
+    T = d_tiles.shape[0]
+    _check_tensor("d_tiles", d_tiles, torch.float32, (T, n ** dims))
+    _check_tensor("g_tiles", g_tiles, torch.float32, (T, r ** dims))
+    return ps, S, T
+
+
+def _ws_size(workspace) -> int:
+    return workspace.numel() * workspace.element_size() if workspace is not None else 0
+
+
 def wino_error_sweep(dims: int, m: int, r: int, point_sets, d_tiles, g_tiles, d_sums, d_maxs,
                      workspace, flags: int = 0, stream=None) -> np.ndarray:
     """point_sets: host [S, n] fp64; d_tiles/g_tiles: CUDA fp32 [T, n^dims]/[T, r^dims];
-    d_sums [S,5] / d_maxs [S,2] CUDA fp64 (accumulated).  Returns per-candidate status."""
-    ps = _np64(point_sets)
-    S = ps.shape[0] if ps.ndim == 2 else 0
+    d_sums [S,5] / d_maxs [S,2] CUDA fp64 (accumulated; NaN rows for rejected candidates).
+    Returns the per-candidate status."""
+    import torch
+    ps, S, T = _sweep_args(dims, m, r, point_sets, d_tiles, g_tiles)
+    _check_tensor("d_sums", d_sums, torch.float64, (S, WINO_SUMS))
+    _check_tensor("d_maxs", d_maxs, torch.float64, (S, WINO_MAXS))
     status = np.zeros(max(S, 1), dtype=np.int32)
-    nt = d_tiles.shape[0]
-    st = load().wino_error_sweep(dims, m, r, ps.ctypes.data_as(_d), S, _ptr(d_tiles), _ptr(g_tiles), nt,
+    st = load().wino_error_sweep(dims, m, r, ps.ctypes.data_as(_d), S, _ptr(d_tiles), _ptr(g_tiles), T,
                                  _ptr(d_sums), _ptr(d_maxs), status.ctypes.data_as(_i), _ptr(workspace),
-                                 workspace.numel() * workspace.element_size() if workspace is not None else 0,
-                                 flags, _stream_ptr(stream))
+                                 _ws_size(workspace), flags, _stream_ptr(stream))
     check(st, "wino_error_sweep")
     return status[:S]
 
 
-def wino_sweep_outputs(dims: int, m: int, r: int, point_sets, d_tiles, g_tiles, d_y, flags: int = 0,
-                       stream=None) -> np.ndarray:
-    """d_y: CUDA fp32 [S, T, m^dims] (overwritten for accepted candidates)."""
-    ps = _np64(point_sets)
-    S = ps.shape[0]
+def wino_sweep_outputs(dims: int, m: int, r: int, point_sets, d_tiles, g_tiles, d_y, workspace=None,
+                       d_sums=None, d_maxs=None, flags: int = 0, stream=None) -> np.ndarray:
+    """The production sweep kernels with the fp32 outputs written to d_y: CUDA fp32
+    [S, T, m^dims] (rows of accepted candidates overwritten).  workspace: uint8 CUDA tensor
+    of wino_error_sweep_workspace_bytes (allocated here when None); d_sums/d_maxs as in
+    wino_error_sweep, or None."""
+    import torch
+    ps, S, T = _sweep_args(dims, m, r, point_sets, d_tiles, g_tiles)
+    _check_tensor("d_y", d_y, torch.float32, (S, T, m ** dims))
+    if (d_sums is None) != (d_maxs is None):
+        raise ValueError("d_sums and d_maxs: both or neither")
+    if d_sums is not None:
+        _check_tensor("d_sums", d_sums, torch.float64, (S, WINO_SUMS))
+        _check_tensor("d_maxs", d_maxs, torch.float64, (S, WINO_MAXS))
+    if workspace is None:
+        workspace = torch.empty(max(1, wino_error_sweep_workspace_bytes(dims, m, r, S, T)), dtype=torch.uint8,
+                                device=d_tiles.device)
     status = np.zeros(max(S, 1), dtype=np.int32)
-    st = load().wino_sweep_outputs(dims, m, r, ps.ctypes.data_as(_d), S, _ptr(d_tiles), _ptr(g_tiles),
-                                   d_tiles.shape[0], _ptr(d_y), status.ctypes.data_as(_i), flags,
-                                   _stream_ptr(stream))
+    st = load().wino_sweep_outputs(dims, m, r, ps.ctypes.data_as(_d), S, _ptr(d_tiles), _ptr(g_tiles), T,
+                                   _ptr(d_y), _ptr(d_sums), _ptr(d_maxs), status.ctypes.data_as(_i),
+                                   _ptr(workspace), _ws_size(workspace), flags, _stream_ptr(stream))
     check(st, "wino_sweep_outputs")
     return status[:S]
 

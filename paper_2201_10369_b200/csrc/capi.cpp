@@ -159,7 +159,8 @@ int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, 
   if (!x || !w || !y || !points) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (N < 0 || C < 1 || H < 1 || W < 1 || K < 0 || r < 1 || m < 1 || pad < 0)
     return set_error(WINO_E_INVALID_ARG, "negative batch / output channels, non-positive size or negative pad");
-  if (flags & ~(WINO_CONV_TF32 | WINO_CONV_3XTF32)) return set_error(WINO_E_INVALID_ARG, "unknown flags");
+  if (flags & ~(WINO_CONV_TF32 | WINO_CONV_3XTF32 | WINO_CONV_SCORE_PER_IMAGE))
+    return set_error(WINO_E_INVALID_ARG, "unknown flags");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
   if (H + 2 * pad < r || W + 2 * pad < r) return set_error(WINO_E_BAD_SHAPE, "empty output");
@@ -200,7 +201,8 @@ static int sweep_common(int dims, int m, int r, const double* point_sets, int n_
   if (m < 1 || r < 1 || n_cand < 0 || n_tiles < 0) return set_error(WINO_E_INVALID_ARG, "bad sizes");
   if (n_cand > 0 && (!point_sets || !cand_status)) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (n_cand > 0 && n_tiles > 0 && (!d_tiles || !g_tiles)) return set_error(WINO_E_INVALID_ARG, "NULL tiles");
-  if (!d_y && n_cand > 0 && (!d_sums || !d_maxs)) return set_error(WINO_E_INVALID_ARG, "NULL stats");
+  if ((d_sums == nullptr) != (d_maxs == nullptr))
+    return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
   if (flags & ~(WINO_SWEEP_NOFMA | WINO_SWEEP_HUFFMAN | WINO_SWEEP_MIXED))
     return set_error(WINO_E_INVALID_ARG, "unknown flags");
   if ((flags & WINO_SWEEP_HUFFMAN) && (flags & WINO_SWEEP_MIXED))
@@ -216,16 +218,23 @@ static int sweep_common(int dims, int m, int r, const double* point_sets, int n_
 int wino_error_sweep(int dims, int m, int r, const double* point_sets, int n_cand, const float* d_tiles,
                      const float* g_tiles, int64_t n_tiles, double* d_sums, double* d_maxs, int* cand_status,
                      void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  if (n_cand > 0 && (!d_sums || !d_maxs)) {
+    reset_launches();
+    return set_error(WINO_E_INVALID_ARG, "NULL stats");
+  }
   return sweep_common(dims, m, r, point_sets, n_cand, d_tiles, g_tiles, n_tiles, d_sums, d_maxs, nullptr,
                       cand_status, workspace, workspace_bytes, flags, stream);
 }
 
 int wino_sweep_outputs(int dims, int m, int r, const double* point_sets, int n_cand, const float* d_tiles,
-                       const float* g_tiles, int64_t n_tiles, float* d_y, int* cand_status, unsigned flags,
-                       void* stream) {
-  if (!d_y && n_cand > 0 && n_tiles > 0) return set_error(WINO_E_INVALID_ARG, "NULL d_y");
-  return sweep_common(dims, m, r, point_sets, n_cand, d_tiles, g_tiles, n_tiles, nullptr, nullptr,
-                      d_y ? d_y : nullptr, cand_status, nullptr, 0, flags, stream);
+                       const float* g_tiles, int64_t n_tiles, float* d_y, double* d_sums, double* d_maxs,
+                       int* cand_status, void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  if (!d_y && n_cand > 0 && n_tiles > 0) {
+    reset_launches();
+    return set_error(WINO_E_INVALID_ARG, "NULL d_y");
+  }
+  return sweep_common(dims, m, r, point_sets, n_cand, d_tiles, g_tiles, n_tiles, d_sums, d_maxs, d_y, cand_status,
+                      workspace, workspace_bytes, flags, stream);
 }
 
 }  // extern "C"

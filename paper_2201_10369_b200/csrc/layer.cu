@@ -493,9 +493,14 @@ __global__ void __launch_bounds__(256, 2) score_kernel(const float* __restrict__
   }
 }
 
+// one warp per statistics row: row b sums entries [b n_entries, (b + 1) n_entries) of the
+// partials (per image: the CTAs of image b; whole batch: one row over every CTA)
 __global__ void score_finalize_kernel(const double* __restrict__ partial, int n_entries, double* d_sums,
                                       double* d_maxs) {
   const int lane = threadIdx.x;
+  partial += (long long)blockIdx.x * n_entries * 8;
+  d_sums += (long long)blockIdx.x * WINO_SUMS;
+  d_maxs += (long long)blockIdx.x * WINO_MAXS;
   double v[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int e = lane; e < n_entries; e += 32) {
 #pragma unroll
@@ -753,8 +758,12 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     const dim3 sg = score_grid(g);
     const auto sk = cfg->sk;
     timed_launch("layer_score", stream, [&] { sk<<<sg, 256, 0, stream>>>(x, w, y, g, partial); });
+    // partials are ordered image-major (blockIdx.z = image), so per-image rows are contiguous
+    const bool per_image = (flags & WINO_CONV_SCORE_PER_IMAGE) != 0;
+    const unsigned rows = per_image ? sg.z : 1u;
+    const int entries = (int)(per_image ? sg.x * sg.y : sg.x * sg.y * sg.z);
     timed_launch("layer_score_finalize", stream, [&] {
-      score_finalize_kernel<<<1, 32, 0, stream>>>(partial, (int)(sg.x * sg.y * sg.z), d_sums, d_maxs);
+      score_finalize_kernel<<<rows, 32, 0, stream>>>(partial, entries, d_sums, d_maxs);
     });
     launches += 2;
   }

@@ -1,38 +1,47 @@
 // Error sweep over candidate point sets (PAPER.md P:465 error protocol, P:472 sweep),
 // sm_100a.  Kernels:
-//   K6  sweep_refs      : y64 = fp64 direct valid correlation of every tile (c-independent,
-//                         once per call) + per-block Σ|y64| / max|y64|
+//   K6  sweep_prep / sweep_refs : y64 = fp64 direct valid correlation of every tile
+//                         (c-independent, once per call) + per-block Σ|y64| / max|y64|;
+//                         sweep_prep also repacks tiles and y64 = hi + lo into coalesced
+//                         pair layouts for the register-resident kernels
 //   K6b sweep_refs_total: fixed-order total of those per-block reference statistics
 //   K7  sweep1d / 2d    : per (candidate, tile) fp32 Winograd, fused in registers, scored
-//                         against y64; per-(candidate, tile-group) partial statistics
+//                         against y64; per-(candidate, tile-group) partial statistics;
+//                         optionally the fp32 outputs (wino_sweep_outputs: same kernels)
 //   K8  sweep_finalize  : fixed-order reduction of the partials, accumulated into d_sums/d_maxs
+//                         (NaN statistics for rejected candidates)
 //
-// Design (DESIGN.md §5.1):
+// Design (DESIGN.md §5):
 //  * Each thread owns TWO tiles and evaluates them as a pair with FFMA2 (fma.rn.f32x2):
 //    both halves use the same warp-uniform coefficient, broadcast from a uniform register
 //    (SASS `FFMA2 R, R.F32x2, UR.F32, R`).  One FFMA2 issue = 64 lane-FMAs, so the FP32
-//    pipe saturates at half the issue slots; the other half carries the fp64 scoring (its
-//    own FP64 pipe), the uniform coefficient loads and the shared-memory traffic.
+//    pipe saturates at half the issue slots.
 //  * Coefficients of up to kParamFloats/per candidates ride in the kernel parameter space
 //    (__grid_constant__); indexing it with the warp-uniform candidate index compiles to
 //    LDCU UR, c[0x0][UR+off].  The host builds chunk k+1's matrices while chunk k runs.
-//  * Structural zeros: a kernel instantiated with zero masks (ZA, ZG, ZB) skips those
-//    terms at compile time; the launcher uses it only when every candidate of the chunk
-//    is exactly zero there (e.g. the {0, ±c, ±1/c, ∞} family: 570 of 834 FMAs remain).
-//    Skipping an exactly-zero term leaves an fmaf chain bit-identical (up to a zero's sign).
-//  * A CTA owns a group of candidates and a range of tile blocks: tiles (and their y64)
-//    are staged in shared memory once per block and reused by every candidate of the
-//    group; per-candidate statistics accumulate in shared memory in tile-block order, so
-//    the partials are few and the reduction order is fixed (bitwise deterministic).
+//  * Structural zeros: a kernel instantiated for a zero family Z (zero_masks.h, generated
+//    from libwino's own builder) skips those terms at compile time; the launcher uses it
+//    only when every candidate of the chunk is exactly zero there (e.g. the
+//    {0, ±c, ±1/c, ∞} family: 570 of 834 FMAs remain).  Skipping an exactly-zero term
+//    leaves an fmaf chain bit-identical (up to a zero's sign) as long as every intermediate
+//    is finite; otherwise some output is non-finite and the careful path re-evaluates with
+//    the DENSE chains (the oracle's, where inf * 0 = NaN).
+//  * A CTA owns a group of candidates and a range of tile blocks; the tiles are loaded once
+//    per block (register kernels: coalesced pair layout from K6) and reused by every
+//    candidate of the group.  Register kernels accumulate each thread's fp32 statistics
+//    per candidate in its own shared-memory slots (no warp reduction inside the candidate
+//    loop) and reduce them in fp64 in a fixed order once per work item; generic kernels
+//    reduce per warp in fp64.  Every reduction order is fixed (bitwise deterministic) and
+//    independent of the candidate sharding.
 //  * Arithmetic is the canonical O5 order: every dot product is an fmaf
 //    chain from +0 in ascending index order, 2D left product first, so outputs are
 //    bit-identical to the oracle.  Rows of V are streamed: for each row i the kernel forms
 //    T1 row i -> U row i, T2 row i -> V row i, Mw row i = U⊙V and accumulates
 //    T3 += Aᵀ[:,i] Mw[i,:] -- per element the same chain as the oracle.
-//  * Scoring: e = (double)y32 − y64; Σ|e|, Σe², max|e| per output (7 instructions).  A
-//    non-finite e makes Σ|e| non-finite; such a warp re-evaluates the candidate with
-//    per-output checks (the rare degenerate-candidate path).  Σ|y64|, max|y64| do not
-//    depend on the candidate and come from K6 (statistics layout, include/wino.h).
+//  * Scoring: e = y32 − y64 per output; Σ|e|, Σe², max|e|.  A non-finite e makes the sums
+//    non-finite; such a candidate is re-evaluated with per-output checks (the rare
+//    degenerate-candidate path; padding tiles excluded).  Σ|y64|, max|y64| do not depend
+//    on the candidate and come from K6 (statistics layout, include/wino.h).
 #include <cmath>
 
 #include "sweep_huff.cuh"
@@ -60,9 +69,10 @@ __global__ void sweep_refs_total_kernel(const double* __restrict__ ref_part, int
 }
 
 // ------------------------------------------------------------------ K8: finalize
-// One warp per accepted candidate: lane l sums tile groups l, l+32, ... in order, then a
-// butterfly; adds the candidate-independent reference statistics (K6b).  Acceptance
-// travels as a bitmask in the parameter space (no host->device copy).
+// One warp per candidate: an accepted candidate's lane l sums tile groups l, l+32, ... in
+// order, then a butterfly, and adds the candidate-independent reference statistics (K6b);
+// a rejected candidate gets NaN statistics (include/wino.h (3)).  Acceptance travels as a
+// bitmask in the parameter space (no host->device copy).
 constexpr int kFinCands = 65536;
 struct OkMask {
   unsigned bits[kFinCands / 32];
@@ -70,10 +80,19 @@ struct OkMask {
 
 __global__ void sweep_finalize_kernel(const double* __restrict__ partial, int n_tgroups, int c0, int n_cand,
                                       const __grid_constant__ OkMask ok, const double* __restrict__ ref_tot,
-                                      double n_outputs, double* __restrict__ d_sums, double* __restrict__ d_maxs) {
+                                      double n_outputs, int has_work, double* __restrict__ d_sums,
+                                      double* __restrict__ d_maxs) {
   const int cl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (cl >= n_cand || !((ok.bits[cl >> 5] >> (cl & 31)) & 1u)) return;
+  if (cl >= n_cand) return;
   const int c = c0 + cl;
+  double* su = d_sums + (long long)c * WINO_SUMS;
+  double* mx = d_maxs + (long long)c * WINO_MAXS;
+  if (!((ok.bits[cl >> 5] >> (cl & 31)) & 1u)) {
+    if (lane < WINO_SUMS) su[lane] = __longlong_as_double(0x7ff8000000000000ll);
+    if (lane < WINO_MAXS) mx[lane] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  if (!has_work) return;   // no tiles: the accepted candidates' statistics are unchanged
   const double* p = partial + (long long)c * n_tgroups * kPartial;
   double s0 = 0.0, s1 = 0.0, m0 = 0.0, nf = 0.0;
   for (int e = lane; e < n_tgroups; e += 32) {
@@ -92,8 +111,6 @@ __global__ void sweep_finalize_kernel(const double* __restrict__ partial, int n_
     nf += __shfl_xor_sync(0xffffffffu, nf, o);
   }
   if (lane == 0) {
-    double* su = d_sums + (long long)c * WINO_SUMS;
-    double* mx = d_maxs + (long long)c * WINO_MAXS;
     su[0] += s0;
     su[1] += s1;
     su[2] += ref_tot[0];
@@ -182,27 +199,25 @@ int per_cand(int m, int r) {
   return m * n + n * r + n * n;
 }
 
-int tiles_per_block(int dims, Layout lay) {
-  if (dims == 1) return kSwThreads * (lay == TSINGLE ? 1 : 2) * kKP1;
-  return kSwThreads * (lay == TSINGLE ? 1 : 2);
+// tiles per tile block of each kernel family
+enum Family { FAM_REG, FAM_PAIR, FAM_SINGLE, FAM_HUFF, FAM_MIXED };
+long long tiles_per_block(int dims, Family f) {
+  switch (f) {
+    case FAM_REG: return dims == 1 ? (long long)kGroupTiles * kKP1 : kGroupTiles;
+    case FAM_PAIR: return 2 * kSwThreads;
+    case FAM_SINGLE: return kSwThreads;
+    case FAM_HUFF: return 2 * kSwThreads;
+    default: return kSwThreads;   // FAM_MIXED
+  }
 }
 
-size_t smem_bytes(int dims, int m, int r, Layout lay) {
-  if (dims == 1) return 0;
-  const int n = m + r - 1;
-  const size_t acc = (size_t)kMaxCpc * 4 * kPartial * 8;
-  if (lay == TPAIR_REG) return (size_t)m * m * 2 * kSwThreads * 8 + acc;   // y64 as hi/lo fp32 pairs
-  const int W = lay == TPAIR ? 2 : 1;
-  return (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)m * m * W * kSwThreads * 8 + acc;
-}
-
-long long n_tblk_of(int dims, Layout lay, int64_t n_tiles) {
-  const int tpb = tiles_per_block(dims, lay);
+long long n_tblk_of(int dims, Family f, int64_t n_tiles) {
+  const long long tpb = tiles_per_block(dims, f);
   return (n_tiles + tpb - 1) / tpb;
 }
 
 // Tile blocks per work item (a tile group).  ~200 tile groups give enough work items to
-// fill the machine; the partition depends only on (n_tiles, kernel layout), so the
+// fill the machine; the partition depends only on (n_tiles, kernel family), so the
 // reduction order (and every statistic) is the same for any candidate sharding.
 int tblk_per_cta(long long n_tblk) {
   const long long target_groups = 200;
@@ -210,25 +225,27 @@ int tblk_per_cta(long long n_tblk) {
 }
 
 struct WsLayout {
-  size_t y64, partial, ref_part, ref_tot, total;
+  size_t y64, dp, gp, yh, yl, partial, ref_part, ref_tot, total;
 };
 
 WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
-  const int dy = c.dims == 1 ? c.m : c.m * c.m;
-  // partial buffer sized for the layout with the most tile groups
+  const int n = c.m + c.r - 1;
+  const int dn = c.dims == 1 ? n : n * n, dg = c.dims == 1 ? c.r : c.r * c.r, dy = c.dims == 1 ? c.m : c.m * c.m;
   long long n_tg = 1;
-  for (Layout lay : {TPAIR, TSINGLE, TPAIR_REG}) {
-    const long long nb = std::max(n_tblk_of(c.dims, lay, n_tiles), 1LL);
+  for (Family f : {FAM_REG, FAM_PAIR, FAM_SINGLE, FAM_HUFF, FAM_MIXED}) {
+    const long long nb = std::max(n_tblk_of(c.dims, f, n_tiles), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }
-  for (long long tpb : {2LL * kSwThreads, (long long)kSwThreads}) {   // Huffman / mixed kernels
-    const long long nb = std::max((long long)((n_tiles + tpb - 1) / tpb), 1LL);
-    n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
-  }
-  const long long n_ref_blocks = (n_tiles + 255) / 256;
+  const long long n_groups = std::max(n_tblk_of(c.dims, FAM_REG, n_tiles), 1LL) * (c.dims == 1 ? kKP1 : 1);
+  const long long n_ref_blocks = std::max((long long)((n_tiles + 255) / 256), n_groups);
+  const size_t pk = (size_t)n_groups * kSwThreads * sizeof(u64);
   WsLayout L;
   L.y64 = 0;
-  L.partial = L.y64 + align_up((size_t)std::max<int64_t>(n_tiles, 1) * dy * sizeof(double), 256);
+  L.dp = L.y64 + align_up((size_t)std::max<int64_t>(n_tiles, 1) * dy * sizeof(double), 256);
+  L.gp = L.dp + align_up(pk * dn, 256);
+  L.yh = L.gp + align_up(pk * dg, 256);
+  L.yl = L.yh + align_up(pk * dy, 256);
+  L.partial = L.yl + align_up(pk * dy, 256);
   L.ref_part = L.partial + align_up((size_t)std::max(n_cand, 1) * n_tg * kPartial * sizeof(double), 256);
   L.ref_tot = L.ref_part + align_up((size_t)std::max(n_ref_blocks, 1LL) * 2 * sizeof(double), 256);
   L.total = L.ref_tot + 256;
@@ -257,7 +274,6 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
                  unsigned flags, cudaStream_t stream) {
   const SweepCfg* c = find_cfg(dims, m, r);
   if (!c) return set_error(WINO_E_UNSUPPORTED, "no sweep kernel for dims=%d m=%d r=%d", dims, m, r);
-  const bool dump = d_y != nullptr;
   const bool huff = (flags & WINO_SWEEP_HUFFMAN) != 0;
   const int nofma = (flags & WINO_SWEEP_NOFMA) ? 1 : 0;
   const bool mixed = (flags & WINO_SWEEP_MIXED) != 0;
@@ -266,7 +282,9 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     return set_error(WINO_E_UNSUPPORTED, "no %s sweep kernel for dims=%d m=%d r=%d",
                      huff ? "Huffman-order" : "mixed-precision", dims, m, r);
   const std::vector<Variant>& variants = c->variants;
-  const Layout lay = variants.back().lay[nofma];
+  const Family fam = huff ? FAM_HUFF : mixed ? FAM_MIXED
+                     : c->lay == TPAIR_REG ? FAM_REG : c->lay == TPAIR ? FAM_PAIR : FAM_SINGLE;
+  const bool packed = fam == FAM_REG;
   const int n = m + r - 1;
   const int per = per_cand(m, r);
   // floats per candidate in the params: Huffman = matrices + programs, mixed = fp64 matrices
@@ -274,37 +292,45 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   int cmax = (huff || mixed) ? std::min(kParamFloats / stride, kMaxCandsLaunch)
                              : sweep_max_cands_per_launch(dims, m, r);
   const int dy = dims == 1 ? m : m * m;
-  const long long tpb_h = huff ? 2 * kSwThreads : kSwThreads;   // tiles per block, Huffman / mixed
-  const long long n_tblk = n_tiles <= 0 ? 0
-                           : (huff || mixed) ? (n_tiles + tpb_h - 1) / tpb_h
-                                             : n_tblk_of(dims, lay, n_tiles);
+  const long long n_tblk = n_tiles <= 0 ? 0 : n_tblk_of(dims, fam, n_tiles);
+  const long long n_groups = n_tblk * (dims == 1 ? kKP1 : 1);   // packed tile groups (FAM_REG)
   const int tpc = tblk_per_cta(std::max(n_tblk, 1LL));
   const int n_tg = (int)((n_tblk + tpc - 1) / tpc);
   const bool work = n_tiles > 0 && n_cand > 0;
 
   const WsLayout L = ws_layout(*c, n_cand, n_tiles);
   char* ws = reinterpret_cast<char*>(workspace);
-  if (!dump && work) {
-    if (!workspace || ws_bytes < L.total)
-      return set_error(WINO_E_WORKSPACE, "sweep workspace %zu < %zu bytes", ws_bytes, L.total);
+  if (work && (!workspace || ws_bytes < L.total))
+    return set_error(WINO_E_WORKSPACE, "sweep workspace %zu < %zu bytes", ws_bytes, L.total);
+  auto at = [&](size_t off) { return work ? ws + off : nullptr; };
+  double* y64 = reinterpret_cast<double*>(at(L.y64));
+  u64* dp = reinterpret_cast<u64*>(at(L.dp));
+  u64* gp = reinterpret_cast<u64*>(at(L.gp));
+  u64* yh = reinterpret_cast<u64*>(at(L.yh));
+  u64* yl = reinterpret_cast<u64*>(at(L.yl));
+  double* partial = reinterpret_cast<double*>(at(L.partial));
+  double* ref_part = reinterpret_cast<double*>(at(L.ref_part));
+  double* ref_tot = reinterpret_cast<double*>(at(L.ref_tot));
+  size_t smem = 0;
+  if (huff) {
+    smem = (size_t)huff_slot_columns(dims, n) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
+           (size_t)kMaxCpc * 4 * kPartial * 8;
+  } else if (mixed) {
+    smem = (size_t)dy * kSwThreads * 8 + (size_t)kMaxCpc * 4 * kPartial * 8;
+  } else if (packed) {
+    smem = (dims == 2 ? (size_t)dy * kSwThreads * 16 : 0) + kStatSmem;
+  } else {
+    const int W = fam == FAM_PAIR ? 2 : 1;
+    smem = (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)dy * W * kSwThreads * 8 +
+           (size_t)kMaxCpc * 4 * kPartial * 8;
   }
-  double* y64 = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.y64);
-  double* partial = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.partial);
-  double* ref_part = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_part);
-  double* ref_tot = (dump || !work) ? nullptr : reinterpret_cast<double*>(ws + L.ref_tot);
-  const size_t smem = huff    ? (size_t)huff_slot_columns(dims, n) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
-                                    (size_t)kMaxCpc * 4 * kPartial * 8
-                      : mixed ? (size_t)dy * kSwThreads * 8 + (size_t)kMaxCpc * 4 * kPartial * 8
-                              : smem_bytes(dims, m, r, lay);
-  if (work && (huff || mixed) && smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)hc->k[dump ? 1 : 0],
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-  }
-  if (work && !huff && !mixed && smem > 48 * 1024) {
-    for (const Variant& v : variants) {
-      cudaError_t e = cudaFuncSetAttribute((const void*)v.k[nofma][dump ? 1 : 0],
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (work && smem > 48 * 1024) {
+    std::vector<SweepKernel> ks;
+    if (hc) ks.push_back(hc->k);
+    else
+      for (const Variant& v : variants) ks.push_back(v.k[nofma]);
+    for (SweepKernel k : ks) {
+      cudaError_t e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return set_error(WINO_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     }
   }
@@ -323,30 +349,34 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   double AT[WINO_MAX_N * WINO_MAX_N], G[WINO_MAX_N * WINO_MAX_N], BT[WINO_MAX_N * WINO_MAX_N];
   int i = 0;
   int status = WINO_OK;
+  // non-zero positions of one fp32 matrix as a 128-bit mask; an entry beyond bit 127
+  // saturates both words ("nothing may be skipped": only the dense variant matches)
+  auto mark = [](uint64_t (&nz)[2], int t) {
+    if (t < 128) nz[t >> 6] |= 1ull << (t & 63);
+    else nz[0] = nz[1] = ~0ull;
+  };
   // Matrices are built chunk by chunk (a2 on the host) while the previous chunk's kernels
   // run: launches are asynchronous, so host construction overlaps device work.
   while (i < n_cand) {
     int nc = 0;
-    uint64_t nzA = 0, nzG = 0, nzB = 0;   // union of non-zero positions over the chunk
+    uint64_t nzA[2] = {0, 0}, nzG[2] = {0, 0}, nzB[2] = {0, 0};   // union over the chunk
     while (i < n_cand && nc < cmax) {
       const int s = build_r64(m, r, point_sets + (size_t)i * n, n, AT, G, BT);
       cand_status[i] = s;
       if (s == WINO_OK) {
         ok[i] = 1;
         float* dst = chunk.data() + (size_t)nc * stride;
-        // non-zero positions; a matrix with more than 64 entries has no specialised
-        // variant, so its mask saturates (all bits set = "nothing may be skipped")
         for (int t = 0; t < m * n; t++) {
           dst[t] = (float)AT[t];
-          if (dst[t] != 0.0f) nzA |= t < 64 ? 1ull << t : ~0ull;
+          if (dst[t] != 0.0f) mark(nzA, t);
         }
         for (int t = 0; t < n * r; t++) {
           dst[m * n + t] = (float)G[t];
-          if (dst[m * n + t] != 0.0f) nzG |= t < 64 ? 1ull << t : ~0ull;
+          if (dst[m * n + t] != 0.0f) mark(nzG, t);
         }
         for (int t = 0; t < n * n; t++) {
           dst[m * n + n * r + t] = (float)BT[t];
-          if (dst[m * n + n * r + t] != 0.0f) nzB |= t < 64 ? 1ull << t : ~0ull;
+          if (dst[m * n + n * r + t] != 0.0f) mark(nzB, t);
         }
         if (mixed) {   // the fp64 matrices themselves (R64, not rounded)
           double* d64 = reinterpret_cast<double*>(dst);
@@ -370,25 +400,42 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     }
     if (nc == 0 || n_tiles <= 0) continue;
     std::copy(chunk.data(), chunk.data() + (size_t)nc * stride, P->v);
-    if (!dump && !refs_done) {
-      const int tpb = 256;
-      const unsigned nb = (unsigned)((n_tiles + tpb - 1) / tpb);
-      const auto refs = c->refs;
-      timed_launch(dims == 1 ? "sweep_refs1d" : "sweep_refs2d", stream, [&] {
-        refs<<<nb, tpb, 0, stream>>>(d_tiles, g_tiles, y64, (long long)n_tiles, ref_part);
-        sweep_refs_total_kernel<<<1, 32, 0, stream>>>(ref_part, (int)nb, ref_tot);
-      });
+    if (!refs_done) {
+      if (packed) {
+        const auto prep = c->prep;
+        timed_launch(dims == 1 ? "sweep_refs1d" : "sweep_refs2d", stream, [&] {
+          prep<<<(unsigned)n_groups, kSwThreads, 0, stream>>>(d_tiles, g_tiles, (long long)n_tiles, dp, gp, yh, yl,
+                                                              ref_part);
+          sweep_refs_total_kernel<<<1, 32, 0, stream>>>(ref_part, (int)n_groups, ref_tot);
+        });
+      } else {
+        const int tpb = 256;
+        const unsigned nb = (unsigned)((n_tiles + tpb - 1) / tpb);
+        const auto refs = find_cfg(dims, m, r)->refs ? find_cfg(dims, m, r)->refs : nullptr;
+        if (!refs) {
+          status = set_error(WINO_E_UNSUPPORTED, "no fp64 reference kernel for this layout");
+          break;
+        }
+        timed_launch(dims == 1 ? "sweep_refs1d" : "sweep_refs2d", stream, [&] {
+          refs<<<nb, tpb, 0, stream>>>(d_tiles, g_tiles, y64, (long long)n_tiles, ref_part);
+          sweep_refs_total_kernel<<<1, 32, 0, stream>>>(ref_part, (int)nb, ref_tot);
+        });
+      }
       launches += 2;
       refs_done = true;
     }
     // most specialised variant whose skipped entries are zero for every candidate
     const Variant* var = &variants.back();
-    for (const Variant& v : variants)
-      if ((v.za & nzA) == 0 && (v.zg & nzG) == 0 && (v.zb & nzB) == 0) {
+    for (const Variant& v : variants) {
+      bool fits = true;
+      for (int w = 0; w < 2; w++)
+        fits = fits && (v.za[w] & nzA[w]) == 0 && (v.zg[w] & nzG[w]) == 0 && (v.zb[w] & nzB[w]) == 0;
+      if (fits) {
         var = &v;
         break;
       }
-    SweepKernel kern = (huff || mixed) ? hc->k[dump ? 1 : 0] : var->k[nofma][dump ? 1 : 0];
+    }
+    SweepKernel kern = hc ? hc->k : var->k[nofma];
     // Work item = (up to cpc candidates, one tile group).  Persistent grid of one wave of
     // resident CTAs walking the items round-robin; cpc is chosen (<= kMaxCpc, larger is
     // better for amortising the tile loads) so the items fill whole rounds of the wave.
@@ -412,6 +459,10 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     args.d = d_tiles;
     args.g = g_tiles;
     args.y64 = y64;
+    args.dp = dp;
+    args.gp = gp;
+    args.yh = yh;
+    args.yl = yl;
     args.ydump = d_y;
     args.partial = partial;
     args.n_tiles = (long long)n_tiles;
@@ -431,7 +482,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
       break;
     }
   }
-  if (status == WINO_OK && !dump && refs_done) {
+  if (status == WINO_OK && d_sums != nullptr && n_cand > 0) {
     const double n_out = (double)n_tiles * dy;
     OkMask* mask = new OkMask;
     for (int c0 = 0; c0 < n_cand && status == WINO_OK; c0 += kFinCands) {
@@ -441,9 +492,10 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
         if (ok[c0 + k]) mask->bits[k >> 5] |= 1u << (k & 31);
       const int threads = 256;
       const int blocks = (int)(((long long)nc * 32 + threads - 1) / threads);
+      const int has_work = refs_done ? 1 : 0;
       timed_launch("sweep_finalize", stream, [&] {
-        sweep_finalize_kernel<<<blocks, threads, 0, stream>>>(partial, n_tg, c0, nc, *mask, ref_tot, n_out, d_sums,
-                                                              d_maxs);
+        sweep_finalize_kernel<<<blocks, threads, 0, stream>>>(partial, n_tg, c0, nc, *mask, ref_tot, n_out, has_work,
+                                                              d_sums, d_maxs);
       });
       launches++;
       cudaError_t e = cudaGetLastError();

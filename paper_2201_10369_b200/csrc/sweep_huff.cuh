@@ -119,7 +119,7 @@ __device__ __forceinline__ void huff_dot_rows(const float* coef, const u64 (&x)[
 }
 
 // smem: slots [huff_slot_columns][kSwThreads] u64, y64 [MM][2][kSwThreads] double, sacc
-template <int DIMS, int M, int R, bool DUMP>
+template <int DIMS, int M, int R>
 __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                                 const __grid_constant__ IdxParam DI) {
   constexpr int N = M + R - 1;
@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
     const int c_begin = cg * a.cands_per_cta;
     const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
     __syncthreads();
-    if (!DUMP)
-      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    __syncthreads();   // zeroed before lane 0 of any warp accumulates
     const int tb_begin = tg * a.tblk_per_cta;
     const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
     for (int tb = tb_begin; tb < tb_end; tb++) {
@@ -167,9 +167,8 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
         for (int h = 0; h < 2; h++) v[h] = ok[h] ? __ldg(a.g + (tile0 + tid + h * kSwThreads) * DG + e) : 0.0f;
         g[e] = Lane<true, true>::pack(v[0], v[1]);
       }
-      if (!DUMP)
 #pragma unroll
-        for (int o = 0; o < DY; o++)
+      for (int o = 0; o < DY; o++)
 #pragma unroll
           for (int h = 0; h < 2; h++)
             sy[(o * 2 + h) * kSwThreads + tid] = ok[h] ? __ldg(a.y64 + (tile0 + tid + h * kSwThreads) * DY + o) : 0.0;
@@ -251,14 +250,15 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
             for (int p = 0; p < M; p++) y[p * M + q] = o[p];
           }
         }
-        if (DUMP) {
+        if (a.ydump != nullptr) {
           float* yd = a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * DY;
 #pragma unroll
           for (int h = 0; h < 2; h++)
             if (ok[h])
 #pragma unroll
               for (int o = 0; o < DY; o++) yd[(tid + h * kSwThreads) * DY + o] = Lane<true, true>::get(y[o], h);
-        } else {
+        }
+        {
           Stat st;
 #pragma unroll
           for (int o = 0; o < DY; o++) {
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
         }
       }
     }
-    if (!DUMP) {
+    {
       __syncthreads();
       for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
         double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
@@ -300,8 +300,7 @@ HuffCfg make_huff_cfg() {
   h.dims = DIMS;
   h.m = M;
   h.r = R;
-  h.k[0] = (SweepKernel)sweep_huff_kernel<DIMS, M, R, false>;
-  h.k[1] = (SweepKernel)sweep_huff_kernel<DIMS, M, R, true>;
+  h.k = (SweepKernel)sweep_huff_kernel<DIMS, M, R>;
   return h;
 }
 

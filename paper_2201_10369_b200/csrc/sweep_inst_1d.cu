@@ -6,11 +6,11 @@ namespace wino {
 
 std::vector<SweepCfg> sweep_cfgs_1d() {
   return {
-      make_cfg<1, 1, 2, TPAIR>(),
-      make_cfg<1, 2, 3, TPAIR>({make_variant<1, 2, 3, TPAIR, kF23A, kF23G, kF23B>()}),
-      make_cfg<1, 3, 3, TPAIR>(),
-      make_cfg<1, 4, 3, TPAIR>({make_variant<1, 4, 3, TPAIR, kF43A, kF43G, kF43B>()}),
-      make_cfg<1, 5, 3, TPAIR>(),
+      make_cfg<1, 1, 2, TPAIR_REG>(),
+      make_cfg<1, 2, 3, TPAIR_REG>({make_variant<1, 2, 3, TPAIR_REG, kZ_F23_C>()}),
+      make_cfg<1, 3, 3, TPAIR_REG>(),
+      make_cfg<1, 4, 3, TPAIR_REG>({make_variant<1, 4, 3, TPAIR_REG, kZ_F43_C>()}),
+      make_cfg<1, 5, 3, TPAIR_REG>(),
   };
 }
 

@@ -5,7 +5,7 @@
 namespace wino {
 
 std::vector<SweepCfg> sweep_cfgs_2d_f43() {
-  return {make_cfg<2, 4, 3, TPAIR_REG>({make_variant<2, 4, 3, TPAIR_REG, kF43A, kF43G, kF43B>()})};
+  return {make_cfg<2, 4, 3, TPAIR_REG>({make_variant<2, 4, 3, TPAIR_REG, kZ_F43_C>()})};
 }
 
 }  // namespace wino

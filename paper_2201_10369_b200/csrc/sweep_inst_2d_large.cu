@@ -6,8 +6,12 @@ namespace wino {
 
 std::vector<SweepCfg> sweep_cfgs_2d_large() {
   return {
-      make_cfg<2, 3, 3, TSINGLE>(), make_cfg<2, 5, 3, TSINGLE>(), make_cfg<2, 6, 3, TSINGLE>(), make_cfg<2, 4, 5, TSINGLE>(), make_cfg<2, 6, 5, TSINGLE>(),
-      make_cfg<2, 7, 3, TSINGLE>(), make_cfg<2, 8, 3, TSINGLE>(),
+      make_cfg<2, 5, 3, TSINGLE>(),
+      make_cfg<2, 6, 3, TSINGLE>({make_variant<2, 6, 3, TSINGLE, kZ_N8_CD>()}),
+      make_cfg<2, 4, 5, TSINGLE>({make_variant<2, 4, 5, TSINGLE, kZ_N8_C1C2_R5>()}),
+      make_cfg<2, 6, 5, TSINGLE>({make_variant<2, 6, 5, TSINGLE, kZ_N10_C1C2_R5>()}),
+      make_cfg<2, 7, 3, TSINGLE>(),
+      make_cfg<2, 8, 3, TSINGLE>({make_variant<2, 8, 3, TSINGLE, kZ_N10_C1C2>()}),
   };
 }
 

@@ -6,8 +6,9 @@ namespace wino {
 
 std::vector<SweepCfg> sweep_cfgs_2d_small() {
   return {
-      make_cfg<2, 1, 2, TPAIR>(),
-      make_cfg<2, 2, 3, TPAIR>({make_variant<2, 2, 3, TPAIR, kF23A, kF23G, kF23B>()}),
+      make_cfg<2, 1, 2, TPAIR_REG>(),
+      make_cfg<2, 2, 3, TPAIR_REG>({make_variant<2, 2, 3, TPAIR_REG, kZ_F23_C>()}),
+      make_cfg<2, 3, 3, TPAIR_REG>(),
   };
 }
 

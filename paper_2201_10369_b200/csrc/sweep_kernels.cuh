@@ -1,4 +1,4 @@
-// Sweep kernel templates (K7) and their registry types; included by sweep.cu and the
+// Sweep kernel templates (K6-K7) and their registry types; included by sweep.cu and the
 // sweep_inst_*.cu translation units, which instantiate disjoint sets of kernels in
 // parallel compilation units.  See sweep.cu for the design notes.
 #pragma once
@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "wino_internal.h"
+#include "zero_masks.h"
 
 namespace wino {
 typedef unsigned long long u64;
@@ -15,8 +16,10 @@ typedef unsigned long long u64;
 constexpr int kSwThreads = 128;        // 4 warps, one per SM sub-partition
 constexpr int kParamFloats = 7424;     // coefficient floats per launch (29696 B)
 constexpr int kMaxCandsLaunch = 512;   // + 2 KB of candidate indices: < 32764 B of params
-constexpr int kMaxCpc = 32;            // candidates per CTA (smem accumulators)
+constexpr int kMaxCpc = 32;            // candidates per CTA work item
 constexpr int kPartial = 4;            // doubles per partial: s0, s1, m0, nonfin
+constexpr int kKP1 = 4;                // 1D: tile pairs per thread and tile block
+constexpr int kGroupTiles = 2 * kSwThreads;   // tiles per packed group (one pair per thread)
 
 struct __align__(16) MatsParam {
   float v[kParamFloats];
@@ -26,15 +29,19 @@ struct IdxParam {
 };
 
 struct SweepArgs {
-  const float* d;
-  const float* g;
-  const double* y64;
-  float* ydump;
+  const float* d;      // raw tiles [n_tiles][n^dims] (generic kernels)
+  const float* g;      // [n_tiles][r^dims]
+  const double* y64;   // [n_tiles][m^dims] fp64 references (generic kernels)
+  const u64* dp;       // packed tile pairs (register kernels, K6 prep): [group][n^dims][128]
+  const u64* gp;       // [group][r^dims][128]
+  const u64* yh;       // [group][m^dims][128]  y64 = hi + lo as fp32 pairs
+  const u64* yl;
+  float* ydump;        // optional fp32 outputs [n_cand_total][n_tiles][m^dims]; NULL = not written
   double* partial;     // [n_cand_total][n_tgroups][kPartial], indexed by global candidate
   long long n_tiles;
   int n_cand;          // candidates in this launch
   int cands_per_cta;
-  int n_tblk;          // tile blocks (kSwThreads * W tiles each)
+  int n_tblk;          // tile blocks
   int tblk_per_cta;    // tile blocks per work item (a tile group)
   int n_tgroups;
   int n_cgroups;       // candidate groups in this launch; work items = n_cgroups * n_tgroups
@@ -106,12 +113,17 @@ struct Lane<false, NOFMA> {
   static __device__ __forceinline__ float get(T v, int) { return v; }
 };
 
-template <uint64_t MASK>
-__device__ __forceinline__ constexpr bool nz(int k) {
-  return ((MASK >> k) & 1ull) == 0ull;
+__device__ __forceinline__ u64 pack2(float a, float b) {
+  u64 p;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
+  return p;
+}
+__device__ __forceinline__ void split2(u64 p, float& a, float& b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
 }
 
 // ------------------------------------------------------------------ statistics
+// Exact fp64 statistics (generic kernels' fast path and every careful path).
 struct Stat {
   // two independent accumulator sets (one per tile of the pair) halve the serial fp64
   // dependency chains; they are combined in a fixed order before the warp reduction
@@ -160,25 +172,17 @@ struct Stat {
   }
 };
 
-// fp32-pair scoring for the register-resident tile-pair kernel: per output pair (the two
+// fp32-pair scoring of the register-resident tile-pair kernels: per output pair (the two
 // tiles of the thread) e = (y32 − hi) − lo with y64 = hi + lo split into fp32 (the first
 // subtraction is exact whenever y32 and hi are within a factor 2, so e carries a relative
-// error <= 2^-23), |e| by clearing the sign bits, Σ|e| and Σe² as FADD2 / FFMA2 pairs,
-// max|e| per half.  8 instructions per output pair instead of 14 for the fp64 path, on
-// the FP32 pipe.  Per thread and candidate 16 pairs are summed in fp32 and per warp 32
-// threads, then fp64 from there on: the statistics stay within ~1e-6 relative of the
-// fp64 definition (tolerance of the north star: 1 %).  Non-finite values fall through to
-// the exact fp64 careful path.
+// error <= 2^-23), |e| by clearing the sign bits, Σ|e| and Σe² as FADD2 / FFMA2, max|e|
+// per half.  Per thread the pair halves are folded once per candidate and tile block and
+// accumulated in fp32 in shared memory (<= 32 x tile blocks per work item terms); the
+// cross-thread reduction is fp64 in a fixed order.  The statistics stay within ~1e-6
+// relative of the fp64 definition (tolerance of the north star: 1 %).  A non-finite sum
+// sends the candidate's work item to the exact fp64 careful path.
 struct Stat32 {
   u64 s0 = 0ull, s1 = 0ull, m0 = 0ull;
-  static __device__ __forceinline__ void split(u64 p, float& a, float& b) {
-    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
-  }
-  static __device__ __forceinline__ u64 join(float a, float b) {
-    u64 p;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(p) : "f"(a), "f"(b));
-    return p;
-  }
   __device__ __forceinline__ void add(u64 y, u64 hi, u64 lo) {
     u64 e, t;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(hi));
@@ -187,59 +191,114 @@ struct Stat32 {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s0) : "l"(s0), "l"(ae));
     asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s1) : "l"(e), "l"(s1));
     float a0, a1, m0a, m0b;
-    split(ae, a0, a1);
-    split(m0, m0a, m0b);
-    m0 = join(fmaxf(m0a, a0), fmaxf(m0b, a1));
+    split2(ae, a0, a1);
+    split2(m0, m0a, m0b);
+    m0 = pack2(fmaxf(m0a, a0), fmaxf(m0b, a1));
   }
-  __device__ __forceinline__ bool finite() const {
-    float a, b, c, d;
-    split(s0, a, b);
-    split(s1, c, d);
-    return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d);
-  }
-  // warp totals (fixed butterfly order) as fp64
-  __device__ __forceinline__ void warp_reduce(double& r0, double& r1, double& rm) const {
+  // the two halves combined (fixed order)
+  __device__ __forceinline__ void fold(float& v0, float& v1, float& vm) const {
     float a, b;
-    split(s0, a, b);
-    float v0 = a + b;
-    split(s1, a, b);
-    float v1 = a + b;
-    split(m0, a, b);
-    float vm = fmaxf(a, b);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-      vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+    split2(s0, a, b);
+    v0 = a + b;
+    split2(s1, a, b);
+    v1 = a + b;
+    split2(m0, a, b);
+    vm = fmaxf(a, b);
+  }
+};
+
+// Shared-memory statistics of the register kernels: per (candidate of the work item, thread)
+// three fp32 accumulators [kMaxCpc][3][kSwThreads] (thread-private slots: no barrier, no
+// warp reduction inside the candidate loop) and a per-candidate "needs the careful path"
+// flag; scratch for the careful path's 4-warp combination.
+constexpr size_t kStatSmem = (size_t)kMaxCpc * 3 * kSwThreads * 4 + kMaxCpc * 4 + 4 * kPartial * 8;
+
+struct SmemStats {
+  float* acc;    // [kMaxCpc][3][kSwThreads]
+  int* flag;     // [kMaxCpc]
+  double* red;   // [4][kPartial]
+  __device__ __forceinline__ static SmemStats at(unsigned char* p) {
+    SmemStats s;
+    s.acc = reinterpret_cast<float*>(p);
+    s.flag = reinterpret_cast<int*>(s.acc + kMaxCpc * 3 * kSwThreads);
+    s.red = reinterpret_cast<double*>(s.flag + kMaxCpc);
+    return s;
+  }
+  // accumulate one (candidate, tile block) contribution of this thread; `first`: the work
+  // item's first tile block (initialise instead of reading)
+  __device__ __forceinline__ void add(int k, bool first, const Stat32& st32) const {
+    float* a = acc + k * 3 * kSwThreads + threadIdx.x;
+    float o0 = 0.0f, o1 = 0.0f, o2 = 0.0f;
+    if (!first) {
+      o0 = a[0];
+      o1 = a[kSwThreads];
+      o2 = a[2 * kSwThreads];
     }
-    r0 = v0;
-    r1 = v1;
-    rm = vm;
+    float v0, v1, vm;
+    st32.fold(v0, v1, vm);
+    if (!(isfinite(v0) && isfinite(v1))) flag[k] = 1;   // idempotent: order-independent
+    a[0] = o0 + v0;
+    a[kSwThreads] = o1 + v1;
+    a[2 * kSwThreads] = fmaxf(o2, vm);
   }
-  // cheaper variant (1D kernel, where the reduction is amortised over fewer tiles): max|e|
-  // >= 0 orders like its bit pattern -> one redux.sync.max.u32; the two sums share one
-  // butterfly (after the xor-16 exchange lanes < 16 carry Σ|e| and lanes >= 16 Σe²).
-  // Results valid in lane 0.
-  __device__ __forceinline__ void warp_reduce_lane0(double& r0, double& r1, double& rm) const {
-    float a, b;
-    split(s0, a, b);
-    const float v0 = a + b;
-    split(s1, a, b);
-    const float v1 = a + b;
-    split(m0, a, b);
-    const unsigned vm = __float_as_uint(fmaxf(a, b));
-    const bool upper = (threadIdx.x & 16) != 0;
-    float v = upper ? v1 : v0;
-    v += __shfl_xor_sync(0xffffffffu, upper ? v0 : v1, 16);
+  // after a barrier: per unflagged candidate k, fp64 fixed-order sum over the 128 threads
+  // -> the (candidate, tile group) partial.  Warp w handles candidates w, w + 4, ...
+  __device__ __forceinline__ void reduce(int ncand, int c_begin, const IdxParam& DI, double* partial, int n_tgroups,
+                                         int tg) const {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = warp; k < ncand; k += 4) {
+      const float* a = acc + k * 3 * kSwThreads;
+      double v0 = 0.0, v1 = 0.0, vm = 0.0;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    r0 = v;
-    r1 = __shfl_sync(0xffffffffu, v, 16);
-    rm = __uint_as_float(__reduce_max_sync(0xffffffffu, vm));
+      for (int j = 0; j < kSwThreads / 32; j++) {
+        v0 += (double)a[lane + 32 * j];
+        v1 += (double)a[kSwThreads + lane + 32 * j];
+        vm = fmax(vm, (double)a[2 * kSwThreads + lane + 32 * j]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        vm = fmax(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+      }
+      if (lane == 0 && flag[k] == 0) {
+        double* pp = partial + ((long long)DI.idx[c_begin + k] * n_tgroups + tg) * kPartial;
+        pp[0] = v0;
+        pp[1] = v1;
+        pp[2] = vm;
+        pp[3] = 0.0;
+      }
+    }
+  }
+  // careful path epilogue: per-thread exact Stat -> warp butterflies -> 4 warps in order
+  // -> the partial (all threads call; contains barriers)
+  __device__ __forceinline__ void write_careful(Stat& st, double* pp) const {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    st.warp_reduce();
+    if (lane == 0) {
+      red[warp * kPartial + 0] = st.s0[0];
+      red[warp * kPartial + 1] = st.s1[0];
+      red[warp * kPartial + 2] = st.m0[0];
+      red[warp * kPartial + 3] = (double)st.nonfin;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
+      for (int w = 0; w < 4; w++) {
+        v[0] += red[w * kPartial + 0];
+        v[1] += red[w * kPartial + 1];
+        v[2] = red[w * kPartial + 2] > v[2] ? red[w * kPartial + 2] : v[2];
+        v[3] += red[w * kPartial + 3];
+      }
+      for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+    }
+    __syncthreads();
   }
 };
 
 // ------------------------------------------------------------------ K6: fp64 references
+// Generic layouts: y64 [n_tiles][m^dims] = fp64 direct valid correlation of every tile
+// (c-independent, once per call) + per-block Σ|y64| / max|y64|.
 template <int DIMS, int M, int R>
 __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict__ d, const float* __restrict__ g,
                                                          double* __restrict__ y64, long long n_tiles,
@@ -296,13 +355,90 @@ __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict
   }
 }
 
-// ------------------------------------------------------------------ K7 (2D)
-// One candidate on this thread's tile pair; scores (or dumps) the M x M outputs.
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+// Register layouts: the same fp64 references, plus the tiles and references repacked into
+// coalesced pairs.  Group G = tiles [256 G, 256 G + 256); element e of lane tid is the u64
+// (tile 256 G + tid, tile 256 G + 128 + tid); y64 is split into fp32 hi = RN32(y64) and
+// lo = RN32(y64 − hi).  Padding tiles (>= n_tiles) are zeros.  One CTA per group; per-CTA
+// Σ|y64|, max|y64| partials in the same fixed order for any candidate sharding.
+template <int DIMS, int M, int R>
+__global__ void __launch_bounds__(kSwThreads) sweep_prep_kernel(const float* __restrict__ d,
+                                                                const float* __restrict__ g, long long n_tiles,
+                                                                u64* __restrict__ dp, u64* __restrict__ gp,
+                                                                u64* __restrict__ yh, u64* __restrict__ yl,
+                                                                double* __restrict__ ref_part) {
+  constexpr int N = M + R - 1;
+  constexpr int DN = DIMS == 1 ? N : N * N, DG = DIMS == 1 ? R : R * R, DY = DIMS == 1 ? M : M * M;
+  const long long grp = blockIdx.x;
+  const int tid = threadIdx.x;
+  double s = 0.0, mx = 0.0;
+  float y_hi[2][DY], y_lo[2][DY];
+#pragma unroll 1
+  for (int h = 0; h < 2; h++) {
+    const long long t = grp * kGroupTiles + h * kSwThreads + tid;
+    const bool ok = t < n_tiles;
+    const float* dt = d + t * DN;
+    const float* gt = g + t * DG;
+#pragma unroll
+    for (int o = 0; o < DY; o++) {
+      const int p = DIMS == 1 ? o : o / M, q = DIMS == 1 ? 0 : o % M;
+      double acc = 0.0;
+      if (ok) {
+        if (DIMS == 1) {
+          for (int j = 0; j < R; j++) acc = __dadd_rn(acc, __dmul_rn((double)gt[j], (double)dt[p + j]));
+        } else {
+          for (int u = 0; u < R; u++)
+            for (int v = 0; v < R; v++)
+              acc = __dadd_rn(acc, __dmul_rn((double)gt[u * R + v], (double)dt[(p + u) * N + q + v]));
+        }
+      }
+      s += fabs(acc);
+      mx = fmax(mx, fabs(acc));
+      y_hi[h][o] = __double2float_rn(acc);
+      y_lo[h][o] = __double2float_rn(acc - (double)y_hi[h][o]);
+    }
+  }
+  const long long t0 = grp * kGroupTiles + tid, t1 = t0 + kSwThreads;
+  const bool ok0 = t0 < n_tiles, ok1 = t1 < n_tiles;
+  for (int e = 0; e < DN; e++)
+    dp[(grp * DN + e) * kSwThreads + tid] = pack2(ok0 ? __ldg(d + t0 * DN + e) : 0.0f, ok1 ? __ldg(d + t1 * DN + e) : 0.0f);
+  for (int e = 0; e < DG; e++)
+    gp[(grp * DG + e) * kSwThreads + tid] = pack2(ok0 ? __ldg(g + t0 * DG + e) : 0.0f, ok1 ? __ldg(g + t1 * DG + e) : 0.0f);
+#pragma unroll
+  for (int o = 0; o < DY; o++) {
+    yh[(grp * DY + o) * kSwThreads + tid] = pack2(y_hi[0][o], y_hi[1][o]);
+    yl[(grp * DY + o) * kSwThreads + tid] = pack2(y_lo[0][o], y_lo[1][o]);
+  }
+  __shared__ double red[2][4];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = s;
+    red[1][tid >> 5] = mx;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 4; w++) {
+      a += red[0][w];
+      b = fmax(b, red[1][w]);
+    }
+    ref_part[grp * 2] = a;
+    ref_part[grp * 2 + 1] = b;
+  }
+}
+
+// ------------------------------------------------------------------ K7 (2D, generic)
+// One candidate on this thread's tile(s); tiles d in shared memory (reused by the CTA's
+// candidates), T2 staged in shared memory.  Scores (fast: add_fast; careful: exact with
+// per-output finiteness, padding tiles excluded) and, if yd != NULL, writes the outputs.
+template <int M, int R, bool PAIR, bool NOFMA, bool CAREFUL, int Z>
 __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T* sd,
                                        typename Lane<PAIR, NOFMA>::T* st2, const double* sy,
                                        const typename Lane<PAIR, NOFMA>::T (&g)[R * R], int tid, Stat& st,
-                                       float* ydump_tile0, long long tile0, long long n_tiles) {
+                                       float* yd, long long tile0, long long n_tiles) {
   using L = Lane<PAIR, NOFMA>;
   using T = typename L::T;
   constexpr int W = L::W;
@@ -319,7 +455,7 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       T acc = L::zero();
 #pragma unroll
       for (int j = 0; j < N; j++)
-        if (nz<ZB>(i * N + j)) acc = L::fma(dc[j], cm[OFF_B + i * N + j], acc);
+        if (nzB<Z>(i * N + j)) acc = L::fma(dc[j], cm[OFF_B + i * N + j], acc);
       st2[(i * N + q) * kSwThreads + tid] = acc;
     }
   }
@@ -337,7 +473,7 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       T acc = L::zero();
 #pragma unroll
       for (int j = 0; j < R; j++)
-        if (nz<ZG>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
+        if (nzG<Z>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
       t1[q] = acc;
     }
     T t2r[N];
@@ -348,20 +484,20 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       T u = L::zero();
 #pragma unroll
       for (int q = 0; q < R; q++)
-        if (nz<ZG>(l * R + q)) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
+        if (nzG<Z>(l * R + q)) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
       // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]
       T v = L::zero();
 #pragma unroll
       for (int q = 0; q < N; q++)
-        if (nz<ZB>(l * N + q)) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
+        if (nzB<Z>(l * N + q)) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
       const T mw = L::mul(u, v);
       // T3[p][l] += Aᵀ[p][i] Mw[i][l]  (ascending i, from +0)
 #pragma unroll
       for (int p = 0; p < M; p++)
-        if (nz<ZA>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
+        if (nzA<Z>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
     }
   }
-  // Y[p][q] = Σ_l T3[p][l] Aᵀ[q][l]; score or dump
+  // Y[p][q] = Σ_l T3[p][l] Aᵀ[q][l]; score (and write)
 #pragma unroll
   for (int p = 0; p < M; p++) {
 #pragma unroll
@@ -369,16 +505,17 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       T y = L::zero();
 #pragma unroll
       for (int l = 0; l < N; l++)
-        if (nz<ZA>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
+        if (nzA<Z>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
       const int o = p * M + q;
 #pragma unroll
       for (int h = 0; h < W; h++) {
-        if (DUMP) {
-          const long long t = tile0 + tid + h * kSwThreads;
-          if (t < n_tiles) ydump_tile0[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
-        } else if (CAREFUL) {
-          if (h == 0) st.template add_careful<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-          else st.template add_careful<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+        const bool ok = tile0 + tid + h * kSwThreads < n_tiles;
+        if (yd != nullptr && ok) yd[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
+        if (CAREFUL) {
+          if (ok) {
+            if (h == 0) st.template add_careful<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+            else st.template add_careful<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+          }
         } else {
           if (h == 0) st.template add_fast<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
           else st.template add_fast<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
@@ -390,7 +527,7 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
 
 // smem: sd [NN][128] T (tiles), st2 [NN][128] T (T2 staging), sy [MM][W][128] double,
 //       sacc [kMaxCpc][4 warps][kPartial] double
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+template <int M, int R, bool PAIR, bool NOFMA, int Z>
 __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                              const __grid_constant__ IdxParam DI) {
   using L = Lane<PAIR, NOFMA>;
@@ -410,55 +547,54 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
   // persistent CTAs walk the (candidate group, tile group) work items round-robin
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-  const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
-  const int c_begin = cg * a.cands_per_cta;
-  const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
-  __syncthreads();  // the previous item's accumulators are flushed
-  if (!DUMP)
+    const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+    const int c_begin = cg * a.cands_per_cta;
+    const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+    __syncthreads();  // the previous item's accumulators are flushed
     for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    __syncthreads();  // zeroed before any warp accumulates (lane 0 of another warp)
 
-  const int tb_begin = tg * a.tblk_per_cta;
-  const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
-  for (int tb = tb_begin; tb < tb_end; tb++) {
-    const long long tile0 = (long long)tb * TPB;
-    __syncthreads();  // previous block's smem no longer in use
-    // Each thread stages its own W tiles: vector loads of the contiguous tile rows, stores
-    // [e][tid] (pairs as 8-byte words) -> conflict-free shared-memory writes.
-    {
-      bool ok[W];
+    const int tb_begin = tg * a.tblk_per_cta;
+    const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+    for (int tb = tb_begin; tb < tb_end; tb++) {
+      const long long tile0 = (long long)tb * TPB;
+      __syncthreads();  // previous block's smem no longer in use
+      // Each thread stages its own W tiles: vector loads of the contiguous tile rows, stores
+      // [e][tid] (pairs as 8-byte words) -> conflict-free shared-memory writes.
+      {
+        bool ok[W];
 #pragma unroll
-      for (int h = 0; h < W; h++) ok[h] = tile0 + tid + h * kSwThreads < a.n_tiles;
-      if constexpr (NN % 4 == 0) {
+        for (int h = 0; h < W; h++) ok[h] = tile0 + tid + h * kSwThreads < a.n_tiles;
+        if constexpr (NN % 4 == 0) {
 #pragma unroll 3
-        for (int e4 = 0; e4 < NN / 4; e4++) {
-          float4 v[W];
+          for (int e4 = 0; e4 < NN / 4; e4++) {
+            float4 v[W];
 #pragma unroll
-          for (int h = 0; h < W; h++)
-            v[h] = ok[h] ? __ldg(reinterpret_cast<const float4*>(a.d + (tile0 + tid + h * kSwThreads) * NN) + e4)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-          if constexpr (PAIR) {
-            sd[(e4 * 4 + 0) * kSwThreads + tid] = L::pack(v[0].x, v[W - 1].x);
-            sd[(e4 * 4 + 1) * kSwThreads + tid] = L::pack(v[0].y, v[W - 1].y);
-            sd[(e4 * 4 + 2) * kSwThreads + tid] = L::pack(v[0].z, v[W - 1].z);
-            sd[(e4 * 4 + 3) * kSwThreads + tid] = L::pack(v[0].w, v[W - 1].w);
-          } else {
-            reinterpret_cast<float*>(sd)[(e4 * 4 + 0) * kSwThreads + tid] = v[0].x;
-            reinterpret_cast<float*>(sd)[(e4 * 4 + 1) * kSwThreads + tid] = v[0].y;
-            reinterpret_cast<float*>(sd)[(e4 * 4 + 2) * kSwThreads + tid] = v[0].z;
-            reinterpret_cast<float*>(sd)[(e4 * 4 + 3) * kSwThreads + tid] = v[0].w;
+            for (int h = 0; h < W; h++)
+              v[h] = ok[h] ? __ldg(reinterpret_cast<const float4*>(a.d + (tile0 + tid + h * kSwThreads) * NN) + e4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            if constexpr (PAIR) {
+              sd[(e4 * 4 + 0) * kSwThreads + tid] = L::pack(v[0].x, v[W - 1].x);
+              sd[(e4 * 4 + 1) * kSwThreads + tid] = L::pack(v[0].y, v[W - 1].y);
+              sd[(e4 * 4 + 2) * kSwThreads + tid] = L::pack(v[0].z, v[W - 1].z);
+              sd[(e4 * 4 + 3) * kSwThreads + tid] = L::pack(v[0].w, v[W - 1].w);
+            } else {
+              reinterpret_cast<float*>(sd)[(e4 * 4 + 0) * kSwThreads + tid] = v[0].x;
+              reinterpret_cast<float*>(sd)[(e4 * 4 + 1) * kSwThreads + tid] = v[0].y;
+              reinterpret_cast<float*>(sd)[(e4 * 4 + 2) * kSwThreads + tid] = v[0].z;
+              reinterpret_cast<float*>(sd)[(e4 * 4 + 3) * kSwThreads + tid] = v[0].w;
+            }
+          }
+        } else {
+#pragma unroll 4
+          for (int e = 0; e < NN; e++) {
+            float v[W];
+#pragma unroll
+            for (int h = 0; h < W; h++) v[h] = ok[h] ? __ldg(a.d + (tile0 + tid + h * kSwThreads) * NN + e) : 0.0f;
+            if constexpr (PAIR) sd[e * kSwThreads + tid] = L::pack(v[0], v[W - 1]);
+            else reinterpret_cast<float*>(sd)[e * kSwThreads + tid] = v[0];
           }
         }
-      } else {
-#pragma unroll 4
-        for (int e = 0; e < NN; e++) {
-          float v[W];
-#pragma unroll
-          for (int h = 0; h < W; h++) v[h] = ok[h] ? __ldg(a.d + (tile0 + tid + h * kSwThreads) * NN + e) : 0.0f;
-          if constexpr (PAIR) sd[e * kSwThreads + tid] = L::pack(v[0], v[W - 1]);
-          else reinterpret_cast<float*>(sd)[e * kSwThreads + tid] = v[0];
-        }
-      }
-      if (!DUMP) {
 #pragma unroll
         for (int h = 0; h < W; h++) {
           const double* ysrc = a.y64 + (tile0 + tid + h * kSwThreads) * MM;
@@ -475,30 +611,30 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
           }
         }
       }
-    }
-    T g[RR];
+      T g[RR];
 #pragma unroll
-    for (int e = 0; e < RR; e++) {
-      float gv[2] = {0.0f, 0.0f};
+      for (int e = 0; e < RR; e++) {
+        float gv[2] = {0.0f, 0.0f};
 #pragma unroll
-      for (int h = 0; h < W; h++) {
-        const long long t = tile0 + tid + h * kSwThreads;
-        if (t < a.n_tiles) gv[h] = a.g[t * RR + e];
+        for (int h = 0; h < W; h++) {
+          const long long t = tile0 + tid + h * kSwThreads;
+          if (t < a.n_tiles) gv[h] = a.g[t * RR + e];
+        }
+        if constexpr (PAIR) g[e] = L::pack(gv[0], gv[1]);
+        else g[e] = gv[0];
       }
-      if constexpr (PAIR) g[e] = L::pack(gv[0], gv[1]);
-      else g[e] = gv[0];
-    }
-    __syncthreads();
+      __syncthreads();
 
-    for (int s = c_begin; s < c_end; s++) {
-      const float* cm = P.v + s * PER;
-      Stat st;
-      float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
-      eval2d<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, sd, st2, sy, g, tid, st, yd, tile0, a.n_tiles);
-      if (!DUMP) {
+      for (int s = c_begin; s < c_end; s++) {
+        const float* cm = P.v + s * PER;
+        Stat st;
+        float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
+        eval2d<M, R, PAIR, NOFMA, false, Z>(cm, sd, st2, sy, g, tid, st, yd, tile0, a.n_tiles);
         if (__any_sync(0xffffffffu, !st.finite())) {
+          // exact per-output path with the dense chains (the oracle's; a skipped zero term
+          // can hide an inf * 0 = NaN of the dense chain), padding tiles excluded
           st = Stat();
-          eval2d<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, sd, st2, sy, g, tid, st, nullptr, tile0, a.n_tiles);
+          eval2d<M, R, PAIR, NOFMA, true, 0>(cm, sd, st2, sy, g, tid, st, yd, tile0, a.n_tiles);
         }
         st.warp_reduce();
         if (lane == 0) {
@@ -510,8 +646,6 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
         }
       }
     }
-  }
-  if (!DUMP) {
     __syncthreads();
     for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
       double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
@@ -525,23 +659,19 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
       double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
       for (int f = 0; f < kPartial; f++) pp[f] = v[f];
     }
-  }
   }  // work items
 }
 
 // ------------------------------------------------------------------ K7 (2D, tiles in registers)
-// Variant of the tile-pair kernel for small n: the thread's two tiles d stay in registers
-// and T2 is formed row by row from them (T2[i][q] = Σ_j Bᵀ[i][j] d[j][q], ascending j), so
-// no candidate-dependent data touches shared memory; only y64 is staged.  Same chains.
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
-__device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
-                                         const typename Lane<PAIR, NOFMA>::T (&d)[(M + R - 1) * (M + R - 1)],
-                                         const typename Lane<PAIR, NOFMA>::T (&g)[R * R], const u64* syh,
-                                         const u64* syl, int tid, Stat& st, Stat32& st32, float* ydump_tile0,
-                                         long long tile0, long long n_tiles) {
-  using L = Lane<PAIR, NOFMA>;
-  using T = typename L::T;
-  constexpr int W = L::W;
+// For small n: the thread's two tiles d stay in registers and T2 is formed row by row from
+// them (T2[i][q] = Σ_j Bᵀ[i][j] d[j][q], ascending j), so no candidate-dependent data
+// touches shared memory; only y64 (hi, lo pairs) is staged.  Same chains as eval2d.
+template <int M, int R, bool NOFMA, bool CAREFUL, int Z>
+__device__ __forceinline__ void eval2d_r(const float* __restrict__ cm, const u64 (&d)[(M + R - 1) * (M + R - 1)],
+                                         const u64 (&g)[R * R], const u64* syh, const u64* syl, int tid, Stat& st,
+                                         Stat32& st32, float* yd, long long tile0, long long n_tiles) {
+  using L = Lane<true, NOFMA>;
+  using T = u64;
   constexpr int N = M + R - 1, MM = M * M;
   constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
   T t3[M][N];
@@ -557,7 +687,7 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
       T acc = L::zero();
 #pragma unroll
       for (int j = 0; j < R; j++)
-        if (nz<ZG>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
+        if (nzG<Z>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
       t1[q] = acc;
     }
     T t2r[N];
@@ -566,7 +696,7 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
       T acc = L::zero();
 #pragma unroll
       for (int j = 0; j < N; j++)
-        if (nz<ZB>(i * N + j)) acc = L::fma(d[j * N + q], cm[OFF_B + i * N + j], acc);
+        if (nzB<Z>(i * N + j)) acc = L::fma(d[j * N + q], cm[OFF_B + i * N + j], acc);
       t2r[q] = acc;
     }
 #pragma unroll
@@ -574,15 +704,15 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
       T u = L::zero();
 #pragma unroll
       for (int q = 0; q < R; q++)
-        if (nz<ZG>(l * R + q)) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
+        if (nzG<Z>(l * R + q)) u = L::fma(t1[q], cm[OFF_G + l * R + q], u);
       T v = L::zero();
 #pragma unroll
       for (int q = 0; q < N; q++)
-        if (nz<ZB>(l * N + q)) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
+        if (nzB<Z>(l * N + q)) v = L::fma(t2r[q], cm[OFF_B + l * N + q], v);
       const T mw = L::mul(u, v);
 #pragma unroll
       for (int p = 0; p < M; p++)
-        if (nz<ZA>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
+        if (nzA<Z>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
     }
   }
 #pragma unroll
@@ -592,22 +722,20 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
       T y = L::zero();
 #pragma unroll
       for (int l = 0; l < N; l++)
-        if (nz<ZA>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
+        if (nzA<Z>(q * N + l)) y = L::fma(t3[p][l], cm[q * N + l], y);
       const int o = p * M + q;
-      if (DUMP) {
+      if (yd != nullptr) {
 #pragma unroll
-        for (int h = 0; h < W; h++) {
-          const long long t = tile0 + tid + h * kSwThreads;
-          if (t < n_tiles) ydump_tile0[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
-        }
-      } else if (CAREFUL) {
+        for (int h = 0; h < 2; h++)
+          if (tile0 + tid + h * kSwThreads < n_tiles) yd[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
+      }
+      if (CAREFUL) {
         // exact fp64 path on y64 = hi + lo (the split is exact in fp64 to 2^-48 relative)
-        const u64 hp = syh[o * kSwThreads + tid], lp = syl[o * kSwThreads + tid];
         float h0, h1, l0, l1;
-        Stat32::split(hp, h0, h1);
-        Stat32::split(lp, l0, l1);
-        st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
-        st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
+        split2(syh[o * kSwThreads + tid], h0, h1);
+        split2(syl[o * kSwThreads + tid], l0, l1);
+        if (tile0 + tid < n_tiles) st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
+        if (tile0 + tid + kSwThreads < n_tiles) st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
       } else {
         st32.add(y, syh[o * kSwThreads + tid], syl[o * kSwThreads + tid]);
       }
@@ -615,131 +743,88 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
   }
 }
 
-// smem: sy [MM][W][128] double, sacc [kMaxCpc][4 warps][kPartial] double
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+// Coalesced loads of the thread's packed tile pair (group grp).
+template <int NN, int RR>
+__device__ __forceinline__ void load_pair2d(const SweepArgs& a, long long grp, int tid, u64 (&d)[NN], u64 (&g)[RR]) {
+#pragma unroll
+  for (int e = 0; e < NN; e++) d[e] = __ldg(a.dp + (grp * NN + e) * kSwThreads + tid);
+#pragma unroll
+  for (int e = 0; e < RR; e++) g[e] = __ldg(a.gp + (grp * RR + e) * kSwThreads + tid);
+}
+
+// smem: syh [MM][128] u64, syl [MM][128] u64, then SmemStats
+template <int M, int R, bool NOFMA, int Z>
 __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                                  const __grid_constant__ IdxParam DI) {
-  using L = Lane<PAIR, NOFMA>;
-  using T = typename L::T;
-  constexpr int W = L::W;
   constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
   constexpr int PER = M * N + N * R + N * N;
-  constexpr int TPB = kSwThreads * W;
-  static_assert(PAIR, "sweep2d_reg_kernel evaluates tile pairs");
   extern __shared__ __align__(16) unsigned char smem[];
   u64* syh = reinterpret_cast<u64*>(smem);            // [MM][128] (hi_A, hi_B)
   u64* syl = syh + MM * kSwThreads;                    // [MM][128] (lo_A, lo_B)
-  double* sacc = reinterpret_cast<double*>(syl + MM * kSwThreads);
+  const SmemStats ss = SmemStats::at(reinterpret_cast<unsigned char*>(syl + MM * kSwThreads));
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
     const int c_begin = cg * a.cands_per_cta;
     const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
-    __syncthreads();  // the previous item's accumulators are flushed
-    if (!DUMP)
-      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    const int ncand = c_end - c_begin;
     const int tb_begin = tg * a.tblk_per_cta;
     const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+    __syncthreads();  // the previous item's statistics have been read
+    if (tid < kMaxCpc) ss.flag[tid] = 0;
+    __syncthreads();
     for (int tb = tb_begin; tb < tb_end; tb++) {
-      const long long tile0 = (long long)tb * TPB;
-      bool ok[W];
-#pragma unroll
-      for (int h = 0; h < W; h++) ok[h] = tile0 + tid + h * kSwThreads < a.n_tiles;
-      T d[NN], g[RR];
-#pragma unroll
-      for (int e = 0; e < NN; e++) {
-        float v[2] = {0.0f, 0.0f};
-#pragma unroll
-        for (int h = 0; h < W; h++)
-          if (ok[h]) v[h] = __ldg(a.d + (tile0 + tid + h * kSwThreads) * NN + e);
-        if constexpr (PAIR) d[e] = L::pack(v[0], v[1]);
-        else d[e] = v[0];
-      }
-#pragma unroll
-      for (int e = 0; e < RR; e++) {
-        float v[2] = {0.0f, 0.0f};
-#pragma unroll
-        for (int h = 0; h < W; h++)
-          if (ok[h]) v[h] = __ldg(a.g + (tile0 + tid + h * kSwThreads) * RR + e);
-        if constexpr (PAIR) g[e] = L::pack(v[0], v[1]);
-        else g[e] = v[0];
-      }
+      const long long tile0 = (long long)tb * kGroupTiles;
+      u64 d[NN], g[RR];
+      load_pair2d<NN, RR>(a, tb, tid, d, g);
       // each thread stages (and later reads) only its own y64 slots: no barrier needed
-      if (!DUMP) {
 #pragma unroll 4
-        for (int o = 0; o < MM; o++) {
-          float hi[2], lo[2];
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const double v = ok[h] ? __ldg(a.y64 + (tile0 + tid + h * kSwThreads) * MM + o) : 0.0;
-            hi[h] = __double2float_rn(v);
-            lo[h] = __double2float_rn(v - (double)hi[h]);
-          }
-          syh[o * kSwThreads + tid] = Stat32::join(hi[0], hi[1]);
-          syl[o * kSwThreads + tid] = Stat32::join(lo[0], lo[1]);
-        }
+      for (int o = 0; o < MM; o++) {
+        syh[o * kSwThreads + tid] = __ldg(a.yh + ((long long)tb * MM + o) * kSwThreads + tid);
+        syl[o * kSwThreads + tid] = __ldg(a.yl + ((long long)tb * MM + o) * kSwThreads + tid);
       }
       for (int s = c_begin; s < c_end; s++) {
         const float* cm = P.v + s * PER;
         Stat st;
         Stat32 st32;
-        float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
-        eval2d_r<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d, g, syh, syl, tid, st, st32, yd, tile0,
-                                                            a.n_tiles);
-        if (!DUMP) {
-          double r0, r1, rm, rn = 0.0;
-          if (__any_sync(0xffffffffu, !st32.finite())) {
-            eval2d_r<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d, g, syh, syl, tid, st, st32, nullptr, tile0,
-                                                                a.n_tiles);
-            st.warp_reduce();
-            r0 = st.s0[0];
-            r1 = st.s1[0];
-            rm = st.m0[0];
-            rn = (double)st.nonfin;
-          } else {
-            st32.warp_reduce(r0, r1, rm);
-          }
-          if (lane == 0) {
-            double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
-            acc[0] += r0;
-            acc[1] += r1;
-            acc[2] = rm > acc[2] ? rm : acc[2];
-            acc[3] += rn;
-          }
-        }
+        float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
+        eval2d_r<M, R, NOFMA, false, Z>(cm, d, g, syh, syl, tid, st, st32, yd, tile0, a.n_tiles);
+        ss.add(s - c_begin, tb == tb_begin, st32);
       }
     }
-    if (!DUMP) {
-      __syncthreads();
-      for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
-        double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
-        for (int w = 0; w < 4; w++) {
-          const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
-          v[0] += acc[0];
-          v[1] += acc[1];
-          v[2] = acc[2] > v[2] ? acc[2] : v[2];
-          v[3] += acc[3];
-        }
-        double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
-        for (int f = 0; f < kPartial; f++) pp[f] = v[f];
+    __syncthreads();
+    ss.reduce(ncand, c_begin, DI, a.partial, a.n_tgroups, tg);
+    // Rare: a candidate whose fp32 sums went non-finite in this work item is re-evaluated
+    // exactly (fp64 statistics per output, dense chains, padding tiles excluded).
+    for (int k = 0; k < ncand; k++) {
+      if (ss.flag[k] == 0) continue;   // uniform: every thread reads the same flag
+      const int s = c_begin + k;
+      const float* cm = P.v + s * PER;
+      Stat st;
+      Stat32 st32;
+      for (int tb = tb_begin; tb < tb_end; tb++) {
+        const long long tile0 = (long long)tb * kGroupTiles;
+        u64 d[NN], g[RR];
+        load_pair2d<NN, RR>(a, tb, tid, d, g);
+        float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
+        eval2d_r<M, R, NOFMA, true, 0>(cm, d, g, a.yh + (long long)tb * MM * kSwThreads,
+                                       a.yl + (long long)tb * MM * kSwThreads, tid, st, st32, yd, tile0, a.n_tiles);
       }
+      ss.write_careful(st, a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial);
     }
   }
 }
 
 // ------------------------------------------------------------------ K7 (1D)
-// Tile pairs in registers; scoring as in the register-resident 2D kernel: fp32 pairs
-// (Stat32) on y64 = hi + lo, exact fp64 careful path for non-finite outputs.
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, bool CAREFUL, uint64_t ZA, uint64_t ZG, uint64_t ZB>
-__device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T (&d)[M + R - 1],
-                                       const typename Lane<PAIR, NOFMA>::T (&g)[R], const u64 (&yh)[M],
-                                       const u64 (&yl)[M], Stat& st, Stat32& st32, float* yd, long long tile0,
-                                       long long n_tiles, int tid) {
-  using L = Lane<PAIR, NOFMA>;
-  using T = typename L::T;
-  constexpr int W = L::W;
+// Tile pairs in registers; scoring as in the register-resident 2D kernel.
+template <int M, int R, bool NOFMA, bool CAREFUL, int Z>
+__device__ __forceinline__ void eval1d(const float* __restrict__ cm, const u64 (&d)[M + R - 1], const u64 (&g)[R],
+                                       const u64 (&yh)[M], const u64 (&yl)[M], Stat& st, Stat32& st32, float* yd,
+                                       long long tile0, long long n_tiles, int tid) {
+  using L = Lane<true, NOFMA>;
+  using T = u64;
   constexpr int N = M + R - 1;
   constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
   T mw[N];
@@ -748,10 +833,10 @@ __device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typen
     T u = L::zero(), v = L::zero();
 #pragma unroll
     for (int j = 0; j < R; j++)
-      if (nz<ZG>(i * R + j)) u = L::fma(g[j], cm[OFF_G + i * R + j], u);
+      if (nzG<Z>(i * R + j)) u = L::fma(g[j], cm[OFF_G + i * R + j], u);
 #pragma unroll
     for (int j = 0; j < N; j++)
-      if (nz<ZB>(i * N + j)) v = L::fma(d[j], cm[OFF_B + i * N + j], v);
+      if (nzB<Z>(i * N + j)) v = L::fma(d[j], cm[OFF_B + i * N + j], v);
     mw[i] = L::mul(u, v);
   }
 #pragma unroll
@@ -759,197 +844,152 @@ __device__ __forceinline__ void eval1d(const float* __restrict__ cm, const typen
     T y = L::zero();
 #pragma unroll
     for (int i = 0; i < N; i++)
-      if (nz<ZA>(p * N + i)) y = L::fma(mw[i], cm[p * N + i], y);
-    if (DUMP) {
+      if (nzA<Z>(p * N + i)) y = L::fma(mw[i], cm[p * N + i], y);
+    if (yd != nullptr) {
 #pragma unroll
-      for (int h = 0; h < W; h++) {
-        const long long t = tile0 + tid + h * kSwThreads;
-        if (t < n_tiles) yd[(tid + h * kSwThreads) * M + p] = L::get(y, h);
-      }
-    } else if (CAREFUL) {
+      for (int h = 0; h < 2; h++)
+        if (tile0 + tid + h * kSwThreads < n_tiles) yd[(tid + h * kSwThreads) * M + p] = L::get(y, h);
+    }
+    if (CAREFUL) {
       float h0, h1, l0, l1;
-      Stat32::split(yh[p], h0, h1);
-      Stat32::split(yl[p], l0, l1);
-      st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
-      st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
+      split2(yh[p], h0, h1);
+      split2(yl[p], l0, l1);
+      if (tile0 + tid < n_tiles) st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
+      if (tile0 + tid + kSwThreads < n_tiles) st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
     } else {
       st32.add(y, yh[p], yl[p]);
     }
   }
 }
 
+// Packed data of sub-block k of tile block tb (group tb * kKP1 + k).
+template <int M, int R>
+__device__ __forceinline__ void load_pair1d(const SweepArgs& a, long long grp, int tid, u64 (&d)[M + R - 1],
+                                            u64 (&g)[R], u64 (&yh)[M], u64 (&yl)[M]) {
+  constexpr int N = M + R - 1;
+#pragma unroll
+  for (int j = 0; j < N; j++) d[j] = __ldg(a.dp + (grp * N + j) * kSwThreads + tid);
+#pragma unroll
+  for (int j = 0; j < R; j++) g[j] = __ldg(a.gp + (grp * R + j) * kSwThreads + tid);
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    yh[j] = __ldg(a.yh + (grp * M + j) * kSwThreads + tid);
+    yl[j] = __ldg(a.yl + (grp * M + j) * kSwThreads + tid);
+  }
+}
+
 // Everything in registers; a CTA walks its tile blocks and, per block, its candidates.
 // Each thread owns kKP1 pairs of tiles, so a candidate's coefficients (uniform registers)
-// and its warp reduction are amortised over 2 * kKP1 tile evaluations.
-constexpr int kKP1 = 4;
-
-template <int M, int R, bool PAIR, bool NOFMA, bool DUMP, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+// are amortised over 2 * kKP1 tile evaluations.  smem: SmemStats.
+template <int M, int R, bool NOFMA, int Z>
 __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                              const __grid_constant__ IdxParam DI) {
-  using L = Lane<PAIR, NOFMA>;
-  using T = typename L::T;
-  static_assert(PAIR, "sweep1d_kernel evaluates tile pairs");
-  constexpr int W = L::W;
   constexpr int N = M + R - 1;
   constexpr int PER = M * N + N * R + N * N;
-  constexpr int TPB = kSwThreads * W * kKP1;
-  __shared__ double sacc[kMaxCpc * 4 * kPartial];
+  constexpr int TPB = kGroupTiles * kKP1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemStats ss = SmemStats::at(smem);
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // persistent CTAs walk the (candidate group, tile group) work items round-robin
+  const int tid = threadIdx.x;
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-  const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
-  const int c_begin = cg * a.cands_per_cta;
-  const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
-  __syncthreads();  // the previous item's accumulators are flushed
-  if (!DUMP)
-    for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
-  __syncthreads();
-
-  const int tb_begin = tg * a.tblk_per_cta;
-  const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
-  for (int tb = tb_begin; tb < tb_end; tb++) {
-    T d[kKP1][N], g[kKP1][R];
-    u64 yh[kKP1][M], yl[kKP1][M];   // y64 = hi + lo as fp32 pairs (tile A, tile B)
+    const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
+    const int c_begin = cg * a.cands_per_cta;
+    const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
+    const int ncand = c_end - c_begin;
+    const int tb_begin = tg * a.tblk_per_cta;
+    const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
+    __syncthreads();
+    if (tid < kMaxCpc) ss.flag[tid] = 0;
+    __syncthreads();
+    for (int tb = tb_begin; tb < tb_end; tb++) {
+      u64 d[kKP1][N], g[kKP1][R], yh[kKP1][M], yl[kKP1][M];
 #pragma unroll
-    for (int k = 0; k < kKP1; k++) {
-      const long long tk0 = (long long)tb * TPB + k * kSwThreads * W;  // tile0 of sub-block k
-      float dv[2][N], gv[2][R];
+      for (int k = 0; k < kKP1; k++) load_pair1d<M, R>(a, (long long)tb * kKP1 + k, tid, d[k], g[k], yh[k], yl[k]);
+      for (int s = c_begin; s < c_end; s++) {
+        const float* cm = P.v + s * PER;
+        Stat st;
+        Stat32 st32;
 #pragma unroll
-      for (int h = 0; h < W; h++) {
-        const long long t = tk0 + tid + h * kSwThreads;
-        const bool ok = t < a.n_tiles;
-#pragma unroll
-        for (int j = 0; j < N; j++) dv[h][j] = ok ? __ldg(a.d + t * N + j) : 0.0f;
-#pragma unroll
-        for (int j = 0; j < R; j++) gv[h][j] = ok ? __ldg(a.g + t * R + j) : 0.0f;
-      }
-#pragma unroll
-      for (int j = 0; j < M; j++) {
-        float hi[2] = {0.0f, 0.0f}, lo[2] = {0.0f, 0.0f};
-#pragma unroll
-        for (int h = 0; h < W; h++) {
-          const long long t = tk0 + tid + h * kSwThreads;
-          const double v = (t < a.n_tiles && !DUMP) ? __ldg(a.y64 + t * M + j) : 0.0;
-          hi[h] = __double2float_rn(v);
-          lo[h] = __double2float_rn(v - (double)hi[h]);
+        for (int k = 0; k < kKP1; k++) {
+          const long long tk0 = (long long)tb * TPB + k * kGroupTiles;
+          float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tk0) * M : nullptr;
+          eval1d<M, R, NOFMA, false, Z>(cm, d[k], g[k], yh[k], yl[k], st, st32, yd, tk0, a.n_tiles, tid);
         }
-        yh[k][j] = Stat32::join(hi[0], hi[1]);
-        yl[k][j] = Stat32::join(lo[0], lo[1]);
-      }
-#pragma unroll
-      for (int j = 0; j < N; j++) {
-        if constexpr (PAIR) d[k][j] = L::pack(dv[0][j], dv[W - 1][j]);
-        else d[k][j] = dv[0][j];
-      }
-#pragma unroll
-      for (int j = 0; j < R; j++) {
-        if constexpr (PAIR) g[k][j] = L::pack(gv[0][j], gv[W - 1][j]);
-        else g[k][j] = gv[0][j];
+        ss.add(s - c_begin, tb == tb_begin, st32);
       }
     }
-    for (int s = c_begin; s < c_end; s++) {
+    __syncthreads();
+    ss.reduce(ncand, c_begin, DI, a.partial, a.n_tgroups, tg);
+    for (int kc = 0; kc < ncand; kc++) {
+      if (ss.flag[kc] == 0) continue;
+      const int s = c_begin + kc;
       const float* cm = P.v + s * PER;
       Stat st;
       Stat32 st32;
-#pragma unroll
-      for (int k = 0; k < kKP1; k++) {
-        const long long tk0 = (long long)tb * TPB + k * kSwThreads * W;
-        float* yd = DUMP ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tk0) * M : nullptr;
-        eval1d<M, R, PAIR, NOFMA, DUMP, false, ZA, ZG, ZB>(cm, d[k], g[k], yh[k], yl[k], st, st32, yd, tk0,
-                                                           a.n_tiles, tid);
-      }
-      if (!DUMP) {
-        double r0, r1, rm, rn = 0.0;
-        if (__any_sync(0xffffffffu, !st32.finite())) {
-#pragma unroll
-          for (int k = 0; k < kKP1; k++)
-            eval1d<M, R, PAIR, NOFMA, false, true, ZA, ZG, ZB>(cm, d[k], g[k], yh[k], yl[k], st, st32, nullptr, 0,
-                                                               a.n_tiles, tid);
-          st.warp_reduce();
-          r0 = st.s0[0];
-          r1 = st.s1[0];
-          rm = st.m0[0];
-          rn = (double)st.nonfin;
-        } else {
-          st32.warp_reduce_lane0(r0, r1, rm);
-        }
-        if (lane == 0) {
-          double* acc = sacc + ((s - c_begin) * 4 + warp) * kPartial;
-          acc[0] += r0;
-          acc[1] += r1;
-          acc[2] = rm > acc[2] ? rm : acc[2];
-          acc[3] += rn;
+      for (int tb = tb_begin; tb < tb_end; tb++) {
+#pragma unroll 1
+        for (int k = 0; k < kKP1; k++) {
+          u64 d[N], g[R], yh[M], yl[M];
+          load_pair1d<M, R>(a, (long long)tb * kKP1 + k, tid, d, g, yh, yl);
+          const long long tk0 = (long long)tb * TPB + k * kGroupTiles;
+          float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tk0) * M : nullptr;
+          eval1d<M, R, NOFMA, true, 0>(cm, d, g, yh, yl, st, st32, yd, tk0, a.n_tiles, tid);
         }
       }
+      ss.write_careful(st, a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial);
     }
   }
-  if (!DUMP) {
-    __syncthreads();
-    for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
-      double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
-      for (int w = 0; w < 4; w++) {
-        const double* acc = sacc + ((s - c_begin) * 4 + w) * kPartial;
-        v[0] += acc[0];
-        v[1] += acc[1];
-        v[2] = acc[2] > v[2] ? acc[2] : v[2];
-        v[3] += acc[3];
-      }
-      double* pp = a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial;
-      for (int f = 0; f < kPartial; f++) pp[f] = v[f];
-    }
-  }
-  }  // work items
 }
 
 typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);
 typedef void (*RefsKernel)(const float*, const float*, double*, long long, double*);
+typedef void (*PrepKernel)(const float*, const float*, long long, u64*, u64*, u64*, u64*, double*);
 
 // Kernel layouts: TPAIR = two tiles per thread (FFMA2 lanes = tiles, coefficients per
-// candidate as uniform registers); TSINGLE = one tile per thread (FFMA), for large n;
-// TPAIR_REG = tile pairs held in registers (sweep2d_reg_kernel), for small n.
+// candidate as uniform registers), tiles in shared memory; TSINGLE = one tile per thread
+// (FFMA), for large n; TPAIR_REG = tile pairs held in registers, packed inputs (K6 prep):
+// the 2D small-n kernel and every 1D kernel.
 enum Layout { TPAIR = 0, TSINGLE = 1, TPAIR_REG = 2 };
 
 struct Variant {
-  uint64_t za, zg, zb;   // structural-zero masks the kernel skips (0 = dense)
-  SweepKernel k[2][2];   // [nofma][dump]
-  Layout lay[2];         // layout of k[nofma][*]
+  int z;                         // structural-zero family (zero_masks.h; 0 = dense)
+  uint64_t za[2], zg[2], zb[2];  // its 128-bit masks (bit k: entry k skipped)
+  SweepKernel k[2];              // [nofma]
+  Layout lay;
 };
 
 struct SweepCfg {
   int dims, m, r;
-  Layout fma_layout;     // layout of the FMA (parity-mode) kernels
-  RefsKernel refs;
-  std::vector<Variant> variants;   // most specialised first, dense last
+  Layout lay;
+  RefsKernel refs;               // generic layouts
+  PrepKernel prep;               // TPAIR_REG
+  std::vector<Variant> variants; // most specialised first, dense last
 };
 
-template <int DIMS, int M, int R, Layout LAY, uint64_t ZA, uint64_t ZG, uint64_t ZB>
+template <int DIMS, int M, int R, Layout LAY, int Z>
 Variant make_variant() {
   Variant v;
-  v.za = ZA;
-  v.zg = ZG;
-  v.zb = ZB;
-  constexpr bool PAIR = LAY != TSINGLE;
-  if constexpr (DIMS == 1) {
-    v.k[0][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, false, false, ZA, ZG, ZB>;
-    v.k[0][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, false, true, ZA, ZG, ZB>;
-    v.k[1][0] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, false, ZA, ZG, ZB>;
-    v.k[1][1] = (SweepKernel)sweep1d_kernel<M, R, PAIR, true, true, ZA, ZG, ZB>;
-    v.lay[0] = v.lay[1] = PAIR ? TPAIR : TSINGLE;
-  } else if constexpr (LAY == TPAIR_REG) {
-    v.k[0][0] = (SweepKernel)sweep2d_reg_kernel<M, R, true, false, false, ZA, ZG, ZB>;
-    v.k[0][1] = (SweepKernel)sweep2d_reg_kernel<M, R, true, false, true, ZA, ZG, ZB>;
-    v.k[1][0] = (SweepKernel)sweep2d_reg_kernel<M, R, true, true, false, ZA, ZG, ZB>;
-    v.k[1][1] = (SweepKernel)sweep2d_reg_kernel<M, R, true, true, true, ZA, ZG, ZB>;
-    v.lay[0] = v.lay[1] = TPAIR_REG;
-  } else {
-    v.k[0][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, false, ZA, ZG, ZB>;
-    v.k[0][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, true, ZA, ZG, ZB>;
-    v.k[1][0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, false, ZA, ZG, ZB>;
-    v.k[1][1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, true, ZA, ZG, ZB>;
-    v.lay[0] = v.lay[1] = PAIR ? TPAIR : TSINGLE;
+  v.z = Z;
+  for (int w = 0; w < 2; w++) {
+    v.za[w] = ZM<Z>::A(w);
+    v.zg[w] = ZM<Z>::G(w);
+    v.zb[w] = ZM<Z>::B(w);
   }
+  if constexpr (Z != 0) static_assert(ZM<Z>::m == M && ZM<Z>::r == R, "zero-mask family of another shape");
+  if constexpr (DIMS == 1) {
+    static_assert(LAY == TPAIR_REG, "1D kernels are register-resident");
+    v.k[0] = (SweepKernel)sweep1d_kernel<M, R, false, Z>;
+    v.k[1] = (SweepKernel)sweep1d_kernel<M, R, true, Z>;
+  } else if constexpr (LAY == TPAIR_REG) {
+    v.k[0] = (SweepKernel)sweep2d_reg_kernel<M, R, false, Z>;
+    v.k[1] = (SweepKernel)sweep2d_reg_kernel<M, R, true, Z>;
+  } else {
+    constexpr bool PAIR = LAY == TPAIR;
+    v.k[0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, Z>;
+    v.k[1] = (SweepKernel)sweep2d_kernel<M, R, PAIR, true, Z>;
+  }
+  v.lay = LAY;
   return v;
 }
 
@@ -959,26 +999,21 @@ SweepCfg make_cfg(std::vector<Variant> specialised = {}) {
   c.dims = DIMS;
   c.m = M;
   c.r = R;
-  c.fma_layout = LAY;
-  c.refs = sweep_refs_kernel<DIMS, M, R>;
+  c.lay = LAY;
+  c.refs = nullptr;
+  c.prep = nullptr;
+  if constexpr (LAY == TPAIR_REG) c.prep = sweep_prep_kernel<DIMS, M, R>;
+  else c.refs = sweep_refs_kernel<DIMS, M, R>;
   c.variants = specialised;
-  c.variants.push_back(make_variant<DIMS, M, R, LAY, 0, 0, 0>());
+  c.variants.push_back(make_variant<DIMS, M, R, LAY, 0>());
   return c;
 }
 
-// Structural-zero masks of the paper's families in canonical order (bit k = row-major
-// entry k of Aᵀ / G / Bᵀ is exactly 0 for every c; generated from oracle R64 over the
-// configs[1] grid, re-checked at run time per chunk and by tests/test_abi.py):
-//   {0, ±c, ±1/c, ∞}, F(4,3):  Aᵀ 0x124920, G 0x18180, Bᵀ 0x56186a861   (570 of 834 FMAs)
-//   {0, ±c, ∞},       F(2,3):  Aᵀ 0x28,     G 0x630,   Bᵀ 0x59a9
-inline constexpr uint64_t kF43A = 0x124920ull, kF43G = 0x18180ull, kF43B = 0x56186a861ull;
-inline constexpr uint64_t kF23A = 0x28ull, kF23G = 0x630ull, kF23B = 0x59a9ull;
-
-
-// Huffman-order (sweep_huff.cuh) and mixed-precision (sweep_mixed.cuh) sweep kernels, [dump]
+// Huffman-order (sweep_huff.cuh) and mixed-precision (sweep_mixed.cuh) sweep kernels
+// (generic layout: raw tiles + fp64 references; always score, write outputs if ydump)
 struct HuffCfg {
   int dims, m, r;
-  SweepKernel k[2];
+  SweepKernel k;
 };
 
 // per-translation-unit registries (sweep_inst_*.cu)

@@ -13,7 +13,7 @@
 namespace wino {
 
 // smem: y64 [DY][kSwThreads] double, sacc
-template <int DIMS, int M, int R, bool DUMP>
+template <int DIMS, int M, int R>
 __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                                  const __grid_constant__ IdxParam DI) {
   constexpr int N = M + R - 1;
@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, co
     const int c_begin = cg * a.cands_per_cta;
     const int c_end = min(a.n_cand, c_begin + a.cands_per_cta);
     __syncthreads();
-    if (!DUMP)
-      for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    for (int k = tid; k < kMaxCpc * 4 * kPartial; k += kSwThreads) sacc[k] = 0.0;
+    __syncthreads();   // zeroed before lane 0 of any warp accumulates
     const int tb_begin = tg * a.tblk_per_cta;
     const int tb_end = min(a.n_tblk, tb_begin + a.tblk_per_cta);
     for (int tb = tb_begin; tb < tb_end; tb++) {
@@ -43,9 +43,8 @@ __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, co
       for (int e = 0; e < DN; e++) d[e] = ok ? (double)__ldg(a.d + t * DN + e) : 0.0;
 #pragma unroll
       for (int e = 0; e < DG; e++) g[e] = ok ? (double)__ldg(a.g + t * DG + e) : 0.0;
-      if (!DUMP)
 #pragma unroll
-        for (int o = 0; o < DY; o++) sy[o * kSwThreads + tid] = ok ? __ldg(a.y64 + t * DY + o) : 0.0;
+      for (int o = 0; o < DY; o++) sy[o * kSwThreads + tid] = ok ? __ldg(a.y64 + t * DY + o) : 0.0;
 
       for (int s = c_begin; s < c_end; s++) {
         const double* AT = PV + s * PER;
@@ -127,13 +126,12 @@ __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, co
               y[p * M + q] = __double2float_rn(acc);
             }
         }
-        if (DUMP) {
-          if (ok) {
-            float* yd = a.ydump + ((long long)DI.idx[s] * a.n_tiles + t) * DY;
+        if (a.ydump != nullptr && ok) {
+          float* yd = a.ydump + ((long long)DI.idx[s] * a.n_tiles + t) * DY;
 #pragma unroll
-            for (int o = 0; o < DY; o++) yd[o] = y[o];
-          }
-        } else {
+          for (int o = 0; o < DY; o++) yd[o] = y[o];
+        }
+        {
           Stat st;
           if (ok)
 #pragma unroll
@@ -149,7 +147,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, co
         }
       }
     }
-    if (!DUMP) {
+    {
       __syncthreads();
       for (int s = c_begin + tid; s < c_end; s += kSwThreads) {
         double v[kPartial] = {0.0, 0.0, 0.0, 0.0};
@@ -173,8 +171,7 @@ HuffCfg make_mixed_cfg() {
   h.dims = DIMS;
   h.m = M;
   h.r = R;
-  h.k[0] = (SweepKernel)sweep_mixed_kernel<DIMS, M, R, false>;
-  h.k[1] = (SweepKernel)sweep_mixed_kernel<DIMS, M, R, true>;
+  h.k = (SweepKernel)sweep_mixed_kernel<DIMS, M, R>;
   return h;
 }
 

@@ -1,7 +1,10 @@
 """c-sweep driver: one process per GPU, candidates sharded in contiguous
 blocks over ranks, per-rank stats written into zero-padded global [S,5] / [S,2] fp64
-buffers, then ONE all_reduce(SUM) + ONE all_reduce(MAX) (NCCL over NVLink).  Zero padding
-makes the reduced statistics bitwise independent of the world size.
+buffers -- views of ONE flat buffer for all the job's sweeps -- then ONE all_reduce(SUM)
+(NCCL over NVLink) per step.  Every candidate row has exactly one owner rank and the other
+ranks hold zeros, so the SUM is exact for the sums AND the maxs (x + 0 = x; NaN rows of
+rejected candidates stay NaN): the reduced statistics are bitwise independent of the world
+size.
 
 The per-rank compute is the C ABI (``wino_error_sweep``); a different ``compute`` can be
 injected for CPU (gloo) tests of the sharding / reduction logic.
@@ -90,6 +93,7 @@ class RankSweep:
     workspace: object
     status: np.ndarray = field(default=None)
     launches: int = 0
+    flat: object = None               # the flat statistics buffer sums/maxs are views of
 
 
 def make_rank_sweep(spec: SweepSpec, rank: int, world: int, device, d_host: np.ndarray, g_host: np.ndarray):
@@ -106,6 +110,23 @@ def make_rank_sweep(spec: SweepSpec, rank: int, world: int, device, d_host: np.n
     return RankSweep(spec, rank, world, lo, hi, sets, d_t, g_t, sums, maxs, ws)
 
 
+def pack_stats(rank_sweeps: Sequence[RankSweep]):
+    """Rebind every sweep's sums [S,5] / maxs [S,2] to contiguous views of one flat fp64
+    buffer (so one collective reduces the whole job).  Returns the buffer."""
+    import torch
+    total = sum(rs.spec.n_cand * 7 for rs in rank_sweeps)
+    flat = torch.zeros(max(total, 1), dtype=torch.float64, device=rank_sweeps[0].sums.device)
+    off = 0
+    for rs in rank_sweeps:
+        S = rs.spec.n_cand
+        rs.sums = flat[off:off + 5 * S].view(S, 5)
+        off += 5 * S
+        rs.maxs = flat[off:off + 2 * S].view(S, 2)
+        off += 2 * S
+        rs.flat = flat
+    return flat
+
+
 def abi_compute(rs: RankSweep, stream=None) -> None:
     """The product compute: wino_error_sweep on this rank's candidate block, writing into
     the global buffers' [lo, hi) rows."""
@@ -120,19 +141,22 @@ def abi_compute(rs: RankSweep, stream=None) -> None:
 
 def run_step(rank_sweeps: Sequence[RankSweep], compute: Callable = abi_compute, group=None,
              reduce: bool = True) -> int:
-    """One step: zero the global buffers, compute every sweep's block, all-reduce.
-    Returns the number of library kernel launches enqueued."""
+    """One step: zero the global buffers, compute every sweep's block, ONE all-reduce(SUM)
+    of the flat statistics buffer (packed on first use).  Returns the number of library
+    kernel launches enqueued."""
     import torch.distributed as dist
+    if any(rs.flat is None for rs in rank_sweeps):
+        pack_stats(rank_sweeps)
+    flats = list({id(rs.flat): rs.flat for rs in rank_sweeps}.values())
+    for f in flats:
+        f.zero_()
     launches = 0
     for rs in rank_sweeps:
-        rs.sums.zero_()
-        rs.maxs.zero_()
         compute(rs)
         launches += rs.launches
     if reduce and dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        for rs in rank_sweeps:
-            dist.all_reduce(rs.sums, op=dist.ReduceOp.SUM, group=group)
-            dist.all_reduce(rs.maxs, op=dist.ReduceOp.MAX, group=group)
+        for f in flats:
+            dist.all_reduce(f, op=dist.ReduceOp.SUM, group=group)
     return launches
 
 

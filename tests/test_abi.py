@@ -61,16 +61,55 @@ def test_builder_bitexact_cfg2_grid():
         _check(4, 3, PP.family_f43(float(c)))
 
 
-def test_builder_bitexact_cfg4_subgrid():
-    g = synth.c_grid(256)
-    for c1 in g[::9]:
-        for c2 in g[::11]:
-            for m, maker in ((4, PP.family_n8_c1c2), (6, PP.family_n10)):
-                try:
-                    pts = maker(float(c1), float(c2))
-                except PP.TemplateError:
+def test_builder_bitexact_cfg4_full_grid():
+    """BASELINE.json configs[3]: every one of the 256 x 256 (c1, c2) point sets of BOTH
+    templates (n = 8 and n = 10, r = 5), memcmp of all three fp64 matrices against the
+    oracle's R64 (SURVEY §8(c) acceptance table).  The points come from the oracle's own
+    template makers; degenerate cells (c1 == c2, c1 == 1/c2, ...) must be rejected by both."""
+    from oracle import points as OP
+    g = [float(c) for c in synth.c_grid(256)]
+    n_checked = n_rejected = 0
+    for c1 in g:
+        for c2 in g:
+            for m, maker in ((4, OP.n8_c1c2), (6, OP.n10_c1c2)):
+                pts = maker(c1, c2)
+                if len(set(pts)) != len(pts):
+                    with pytest.raises(_lib.WinoError):
+                        api.wino_points_to_matrices(m, 5, pts)
+                    n_rejected += 1
                     continue
                 _check(m, 5, pts)
+                n_checked += 1
+    assert n_checked + n_rejected == 2 * 256 * 256 and n_checked > 2 * 65000
+
+
+def test_zero_masks_header_rederived():
+    """csrc/zero_masks.h (the structural zeros the sweep kernels skip at compile time) is
+    exactly what libwino's own builder gives over the configs' grids (tools/gen_zero_masks.py);
+    and each family's mask is a true zero pattern of the oracle's R64 matrices at sampled
+    parameters (an independent check that no skipped entry is ever non-zero)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gen_zero_masks", os.path.join(ROOT, "tools", "gen_zero_masks.py"))
+    gz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gz)
+    text = open(gz.HEADER).read()
+    assert gz.parse(text) == gz.derive(step2=1)
+    assert gz.render(gz.derive(step2=1)) == text
+    from oracle import points as OP
+    makers = {"f23_c": OP.f23_c, "f43_c": OP.f43_c, "n8_cd": OP.n8_cd, "n8_c1c2_r5": OP.n8_c1c2,
+              "n10_c1c2_r5": OP.n10_c1c2, "n10_c1c2": OP.n10_c1c2}
+    masks = gz.parse(text)
+    rng = np.random.default_rng(5)
+    for fid, name, m, r, _, npar, _ in gz.FAMILIES:
+        for _ in range(25):
+            p = tuple(float(v) for v in np.exp(rng.uniform(np.log(0.05), np.log(20), npar)))
+            pts = makers[name](*p)
+            if len(set(pts)) != len(pts):
+                continue
+            for z, M in zip(masks[fid], r64.build_r64(m, r, pts)):
+                flat = np.asarray(M).ravel()
+                skipped = [k for k in range(flat.size) if (z >> k) & 1]
+                assert np.all(flat[skipped] == 0.0), (name, p)
 
 
 def test_builder_bitexact_random_sets():
@@ -117,7 +156,7 @@ def test_builder_errors(m, r, pts, status):
 
 
 def test_supported_table():
-    assert api.wino_supported(2, 4, 3) and api.wino_supported(1, 4, 3)
+    assert api.wino_supported(2, 4, 3) and api.wino_supported(1, 4, 3) and api.wino_supported(2, 3, 3)
     assert api.wino_supported(0, 6, 3) and api.wino_supported(0, 2, 3)
     assert not api.wino_supported(3, 4, 3)
 

@@ -25,13 +25,20 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def _gpu_outputs(dims, m, r, sets, d, g, flags=0):
+def _gpu_outputs(dims, m, r, sets, d, g, flags=0, with_stats=False):
+    """The production sweep kernels with the output store enabled (wino_sweep_outputs);
+    with_stats: also the statistics of the same launch."""
     from paper_2201_10369_b200 import api
     torch = _torch()
     S, T = len(sets), d.shape[0]
     y = torch.full((S, T, m ** dims), float("nan"), dtype=torch.float32, device="cuda")
-    st = api.wino_sweep_outputs(dims, m, r, np.array(sets), _dev(d), _dev(g), y, flags=flags)
+    sums = torch.zeros((S, 5), dtype=torch.float64, device="cuda") if with_stats else None
+    maxs = torch.zeros((S, 2), dtype=torch.float64, device="cuda") if with_stats else None
+    st = api.wino_sweep_outputs(dims, m, r, np.array(sets), _dev(d), _dev(g), y, d_sums=sums, d_maxs=maxs,
+                                flags=flags)
     torch.cuda.synchronize()
+    if with_stats:
+        return st, y.cpu().numpy(), sums.cpu().numpy(), maxs.cpu().numpy()
     return st, y.cpu().numpy()
 
 
@@ -140,19 +147,23 @@ def test_exact_integer_special_case(dims):
 
 
 def test_rejected_candidates_and_accumulation():
+    """A rejected candidate does not fail the call; its statistics rows become NaN (include/
+    wino.h (3)); accepted rows accumulate over calls."""
     torch = _torch()
     sets = [OP.f43_c(1.7), [0.0, 1.0, 1.0, -1.0, 2.0, INF], [math.nan] * 6, OP.f43_c(0.9)]
     d, g = synth.random_tiles(3001, 2, 6, 3, "uniform", seed=15)
     st, s, mx = _gpu_stats(2, 4, 3, sets, d, g)
     assert st.tolist() == [0, 3, 5, 0]
-    assert np.all(s[1:3] == 0) and np.all(mx[1:3] == 0)
+    assert np.all(np.isnan(s[1:3])) and np.all(np.isnan(mx[1:3]))
     s_ref, m_ref, _ = ref.sweep(2, 4, 3, [sets[0], sets[3]], d, g)
     _assert_stats_close(s[[0, 3]], mx[[0, 3]], s_ref, m_ref)
-    # second call accumulates
+    # second call accumulates into the accepted rows; rejected rows stay NaN
     sums = torch.from_numpy(s).cuda()
     maxs = torch.from_numpy(mx).cuda()
     _, s2, m2 = _gpu_stats(2, 4, 3, sets, d, g, sums=sums, maxs=maxs)
-    assert np.allclose(s2, 2 * s, rtol=1e-15) and np.array_equal(m2, mx)
+    ok = [0, 3]
+    assert np.allclose(s2[ok], 2 * s[ok], rtol=1e-15) and np.array_equal(m2[ok], mx[ok])
+    assert np.all(np.isnan(s2[1:3])) and np.all(np.isnan(m2[1:3]))
 
 
 def test_empty_inputs():
@@ -166,7 +177,13 @@ def test_empty_inputs():
     st = api.wino_error_sweep(2, 4, 3, np.array([OP.f43_c(1.5), OP.f43_c(2.5)]), d, g, sums, maxs, ws)
     torch.cuda.synchronize()
     assert st.tolist() == [0, 0] and float(sums.abs().sum()) == 0.0
-    st = api.wino_error_sweep(2, 4, 3, np.zeros((0, 6)), d, g, sums, maxs, ws)
+    # no tiles: a rejected candidate still gets NaN rows, the accepted one is untouched
+    st = api.wino_error_sweep(2, 4, 3, np.array([OP.f43_c(1.5), [0.0, 1.0, 1.0, -1.0, 2.0, INF]]), d, g, sums,
+                              maxs, ws)
+    torch.cuda.synchronize()
+    s = sums.cpu().numpy()
+    assert st.tolist() == [0, 3] and np.all(s[0] == 0) and np.all(np.isnan(s[1]))
+    st = api.wino_error_sweep(2, 4, 3, np.zeros((0, 6)), d, g, sums[:0], maxs[:0], ws)
     assert st.size == 0
 
 
@@ -198,3 +215,59 @@ def test_full_size_cfg2_sampled(dims):
     s_ref, m_ref, _ = ref.sweep(dims, 4, 3, [sets[i] for i in pick], d, g)
     _assert_stats_close(s[pick], mx[pick], s_ref, m_ref)
     assert np.all(s[:, 3] == 100_000 * 4 ** dims)
+
+
+@pytest.mark.parametrize("dims", [2, 1])
+def test_production_outputs_full_tiles(dims):
+    """Per-element parity of the PRODUCTION kernels (the bench's configuration: the
+    zero-skipping {0,±c,±1/c,∞} instantiation, 100k tiles) with the output store enabled,
+    plus the statistics of the same launch, against the oracle."""
+    cs = [float(c) for c in synth.c_grid()[::273]]
+    sets = [OP.f43_c(c) for c in cs]
+    d, g = synth.random_tiles(100_000, dims, 6, 3, "normal", seed=21)
+    st, y, s, mx = _gpu_outputs(dims, 4, 3, sets, d, g, with_stats=True)
+    assert np.all(st == 0)
+    s_ref, m_ref, y_ref = ref.sweep(dims, 4, 3, sets, d, g, n_dump=d.shape[0])
+    assert np.array_equal(y, y_ref)
+    _assert_stats_close(s, mx, s_ref, m_ref)
+
+
+def _overflow_sets(maker_name):
+    """Normal candidates interleaved with ones whose fp32 matrices overflow (inf entries /
+    inf intermediates): c in {1e-19, 1e19} overflow Aᵀ and Bᵀ, c = 1e12, 3e9 overflow
+    intermediates only."""
+    normal = [0.3, 0.7, 1.6, 2.4, 5.0]
+    bad = [1e19, 1e-19, 1e12, 3e9]
+    cs = []
+    for i in range(max(len(normal), len(bad))):
+        if i < len(normal):
+            cs.append(normal[i])
+        if i < len(bad):
+            cs.append(bad[i])
+    if maker_name == "f43":
+        return [OP.f43_c(c) for c in cs]
+    return [OP.n8_cd(c, 1.003) for c in cs]
+
+
+@pytest.mark.parametrize("dims,m,r,fam", [(2, 4, 3, "f43"), (1, 4, 3, "f43"), (2, 6, 3, "n8cd"), (1, 6, 3, "n8cd")])
+def test_nonfinite_candidates_isolated(dims, m, r, fam):
+    """Overflowing candidates mixed with normal ones in ONE launch, ragged tile count: the
+    careful (exact, dense-chain) path must reproduce the oracle's n_nonfinite / n_scored and
+    must not disturb the neighbouring candidates' statistics; outputs (NaN/inf included)
+    equal the oracle's element by element."""
+    sets = _overflow_sets(fam)
+    n = m + r - 1
+    d, g = synth.random_tiles(6007, dims, n, r, "uniform", seed=22)
+    st, y, s, mx = _gpu_outputs(dims, m, r, sets, d, g, with_stats=True)
+    assert np.all(st == 0)
+    s_ref, m_ref, y_ref = ref.sweep(dims, m, r, sets, d, g, n_dump=d.shape[0])
+    assert np.array_equal(y, y_ref, equal_nan=True)
+    assert np.any(s_ref[:, 4] > 0), "the test needs candidates with non-finite outputs"
+    assert np.array_equal(s[:, 3], s_ref[:, 3]) and np.array_equal(s[:, 4], s_ref[:, 4])
+    fin = s_ref[:, 3] > 0
+    assert np.array_equal(mx[:, 1], m_ref[:, 1])
+    assert np.all(np.abs(s[fin, 0] / s_ref[fin, 0] - 1) < RTOL_SUM)
+    assert np.all(np.abs(mx[fin, 0] / m_ref[fin, 0] - 1) <= RTOL_MAX)
+    # the statistics-only call (output store off: the same kernel) gives bitwise the same
+    st2, s2, m2 = _gpu_stats(dims, m, r, sets, d, g)
+    assert np.array_equal(s2, s, equal_nan=True) and np.array_equal(m2, mx, equal_nan=True)

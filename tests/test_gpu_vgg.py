@@ -17,11 +17,11 @@ def test_vgg16_two_images():
     x, ws = synth.vgg16_inputs(2, seed=0)
     pts = OP.n8_cd(2.0, 1.003)
     dev = torch.device("cuda", 0)
-    out, s, mx, ys = network.vgg16_forward(torch.from_numpy(x).to(dev), [torch.from_numpy(w).to(dev) for w in ws],
-                                           pts, m=6, score=True, keep=True)
+    out, s, mx, ys, _ = network.vgg16_forward(torch.from_numpy(x).to(dev),
+                                              [torch.from_numpy(w).to(dev) for w in ws], pts, m=6, score=True,
+                                              keep=True)
     torch.cuda.synchronize()
     ys_ref, s_ref, m_ref = ON.vgg16(x, ws, pts, m=6)
-    s, mx = s.cpu().numpy(), mx.cpu().numpy()
     for li in range(13):
         assert np.array_equal(ys[li].cpu().numpy(), ys_ref[li]), li
         assert s[li, 3] == s_ref[li, 3] and s[li, 4] == s_ref[li, 4]
@@ -48,19 +48,19 @@ def test_relu_pool_exact():
 
 def test_resnet20_like_stack_chebyshev_and_n5():
     """NEXT row N4 stack (CIFAR-shaped synthetic inputs): bit-identical to the oracle chain
-    for the Chebyshev nodes and the n = 5 proposed set, first 8 layers, 3 images."""
+    for the Chebyshev nodes (the oracle's own generator) and the n = 5 proposed set, first 8
+    layers, 3 images."""
     import torch
-    from paper_2201_10369_b200 import network, points as PP
+    from paper_2201_10369_b200 import network
     layers = network.RESNET20_LIKE[:8]
     x, ws = synth.stack_inputs(layers, 3, seed=1)
     dev = torch.device("cuda", 0)
-    for m, pts in ((2, PP.chebyshev(4)), (3, sorted([0.0, 1.0, -1.0, -2.0]) + [float("inf")]),
-                   (6, PP.chebyshev(8))):
-        _, s, mx, ys = network.stack_forward(layers, torch.from_numpy(x).to(dev),
-                                             [torch.from_numpy(w).to(dev) for w in ws], pts, m=m, keep=True)
+    for m, pts in ((2, OP.chebyshev(4)), (3, sorted([0.0, 1.0, -1.0, -2.0]) + [float("inf")]),
+                   (6, OP.chebyshev(8))):
+        _, s, mx, ys, _ = network.stack_forward(layers, torch.from_numpy(x).to(dev),
+                                                [torch.from_numpy(w).to(dev) for w in ws], pts, m=m, keep=True)
         torch.cuda.synchronize()
         ys_ref, s_ref, m_ref = ON.stack(layers, x, ws, pts, m=m)
-        s = s.cpu().numpy()
         for li in range(len(layers)):
             assert np.array_equal(ys[li].cpu().numpy(), ys_ref[li]), (m, li)
             assert abs(s[li, 0] / s_ref[li, 0] - 1) < 1e-9

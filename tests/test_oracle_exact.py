@@ -202,3 +202,37 @@ def test_multiplies_per_output_table1():
         for n, v in gold[key].items():
             val = float(exact.multiplies_per_output(int(n), kk, 2))
             assert round(val, 2) == v, (n, kk, val)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 8, 9, 10, 11])
+def test_chebyshev_nodes_are_roots_of_Tq(n):
+    """Oracle Chebyshev generator (reading X24): the n - 1 finite nodes are the roots
+    of the Chebyshev polynomial T_{n-1} (three-term recurrence, a textbook fact independent
+    of the cosine formula), distinct, exactly symmetric (x and -x both present, 0 for odd
+    counts), within 4 ulp of 1 of cos((2k-1) pi / (2q)) (the mirrored half differs from the
+    direct formula only by the rounding of its argument), and inf last."""
+    import math
+    from oracle import points as OP
+    pts = OP.chebyshev(n)
+    assert len(pts) == n and pts[-1] == math.inf
+    fin = pts[:-1]
+    q = n - 1
+    assert len(set(fin)) == q and fin == sorted(fin)
+    assert sorted(-v for v in fin) == fin
+    for x in fin:
+        t0, t1 = 1.0, x
+        for _ in range(q - 1):
+            t0, t1 = t1, 2 * x * t1 - t0
+        assert abs(t1) < 1e-12 * q
+    direct = sorted(math.cos((2 * k - 1) * math.pi / (2 * q)) for k in range(1, q + 1))
+    for a, b in zip(fin, direct):
+        assert abs(a - b) <= 4 * math.ulp(1.0)
+
+
+def test_chebyshev_product_template_matches_oracle():
+    """The product's template (paper_2201_10369_b200.points.chebyshev) and the oracle's
+    generator agree bit for bit (GPU tests feed the oracle's sets to both sides)."""
+    from oracle import points as OP
+    from paper_2201_10369_b200 import points as PP
+    for n in range(3, 12):
+        assert PP.chebyshev(n) == OP.chebyshev(n)

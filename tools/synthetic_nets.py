@@ -48,8 +48,7 @@ def main():
     out = {"workload": f"ResNet-20-shaped 3x3 stack, {args.images} synthetic 32x32x3 images", "rows": []}
     for n, fams in families().items():
         for name, pts in fams.items():
-            _, s, _, _ = network.stack_forward(layers, xd, wd, pts, m=n - 2, score=True)
-            s = s.cpu().numpy()
+            _, s, _, _, _ = network.stack_forward(layers, xd, wd, pts, m=n - 2, score=True)
             out["rows"].append({"n": n, "points": name, "normalized_l1": network.normalized_l1(s, args.images),
                                 "mean_abs_err": float(s[:, 0].sum() / s[:, 3].sum()),
                                 "nonfinite": int(s[:, 4].sum())})
