@@ -580,9 +580,12 @@ dim3 score_grid(const Geo& g) {
               (unsigned)g.N);
 }
 
+// F(m x m, 3 x 3) for m = 2..8 (n = 4..10: the paper's T7-T9 sizes) and the
+// 5 x 5 kernels of configs[3]
 const LayerCfg kLayerCfgs[] = {
     make_layer_cfg<2, 3>(), make_layer_cfg<3, 3>(), make_layer_cfg<4, 3>(), make_layer_cfg<5, 3>(),
-    make_layer_cfg<6, 3>(), make_layer_cfg<2, 5>(), make_layer_cfg<4, 5>(), make_layer_cfg<6, 5>(),
+    make_layer_cfg<6, 3>(), make_layer_cfg<7, 3>(), make_layer_cfg<8, 3>(),
+    make_layer_cfg<2, 5>(), make_layer_cfg<4, 5>(), make_layer_cfg<6, 5>(),
 };
 
 const LayerCfg* find_layer(int m, int r) {

@@ -127,7 +127,8 @@ namespace {
 const std::vector<SweepCfg>& cfgs() {
   static const std::vector<SweepCfg> v = [] {
     std::vector<SweepCfg> all;
-    for (auto f : {sweep_cfgs_1d, sweep_cfgs_1d_large, sweep_cfgs_2d_small, sweep_cfgs_2d_f43, sweep_cfgs_2d_large})
+    for (auto f : {sweep_cfgs_1d, sweep_cfgs_1d_large, sweep_cfgs_2d_small, sweep_cfgs_2d_f43, sweep_cfgs_2d_mid,
+                   sweep_cfgs_2d_large})
       for (auto& c : f()) all.push_back(c);
     return all;
   }();
@@ -200,10 +201,11 @@ int per_cand(int m, int r) {
 }
 
 // tiles per tile block of each kernel family
-enum Family { FAM_REG, FAM_PAIR, FAM_SINGLE, FAM_HUFF, FAM_MIXED };
+enum Family { FAM_REG, FAM_REG1, FAM_PAIR, FAM_SINGLE, FAM_HUFF, FAM_MIXED };
 long long tiles_per_block(int dims, Family f) {
   switch (f) {
     case FAM_REG: return dims == 1 ? (long long)kGroupTiles * kKP1 : kGroupTiles;
+    case FAM_REG1: return kSwThreads;
     case FAM_PAIR: return 2 * kSwThreads;
     case FAM_SINGLE: return kSwThreads;
     case FAM_HUFF: return 2 * kSwThreads;
@@ -225,23 +227,26 @@ int tblk_per_cta(long long n_tblk) {
 }
 
 struct WsLayout {
-  size_t y64, dp, gp, yh, yl, partial, ref_part, ref_tot, total;
+  size_t y64, y64t, dp, gp, yh, yl, partial, ref_part, ref_tot, total;
 };
 
 WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
   const int n = c.m + c.r - 1;
   const int dn = c.dims == 1 ? n : n * n, dg = c.dims == 1 ? c.r : c.r * c.r, dy = c.dims == 1 ? c.m : c.m * c.m;
   long long n_tg = 1;
-  for (Family f : {FAM_REG, FAM_PAIR, FAM_SINGLE, FAM_HUFF, FAM_MIXED}) {
+  for (Family f : {FAM_REG, FAM_REG1, FAM_PAIR, FAM_SINGLE, FAM_HUFF, FAM_MIXED}) {
     const long long nb = std::max(n_tblk_of(c.dims, f, n_tiles), 1LL);
     n_tg = std::max(n_tg, (nb + tblk_per_cta(nb) - 1) / tblk_per_cta(nb));
   }
-  const long long n_groups = std::max(n_tblk_of(c.dims, FAM_REG, n_tiles), 1LL) * (c.dims == 1 ? kKP1 : 1);
+  const long long n_groups = std::max(std::max(n_tblk_of(c.dims, FAM_REG, n_tiles), 1LL) * (c.dims == 1 ? kKP1 : 1),
+                                      n_tblk_of(c.dims, FAM_REG1, n_tiles));
   const long long n_ref_blocks = std::max((long long)((n_tiles + 255) / 256), n_groups);
   const size_t pk = (size_t)n_groups * kSwThreads * sizeof(u64);
   WsLayout L;
   L.y64 = 0;
-  L.dp = L.y64 + align_up((size_t)std::max<int64_t>(n_tiles, 1) * dy * sizeof(double), 256);
+  const long long t_pad = ((std::max<int64_t>(n_tiles, 1) + 255) / 256) * 256;   // refs kernel grid
+  L.y64t = L.y64 + align_up((size_t)std::max<int64_t>(n_tiles, 1) * dy * sizeof(double), 256);
+  L.dp = L.y64t + align_up((size_t)t_pad * dy * sizeof(double), 256);
   L.gp = L.dp + align_up(pk * dn, 256);
   L.yh = L.gp + align_up(pk * dg, 256);
   L.yl = L.yh + align_up(pk * dy, 256);
@@ -283,8 +288,9 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
                      huff ? "Huffman-order" : "mixed-precision", dims, m, r);
   const std::vector<Variant>& variants = c->variants;
   const Family fam = huff ? FAM_HUFF : mixed ? FAM_MIXED
-                     : c->lay == TPAIR_REG ? FAM_REG : c->lay == TPAIR ? FAM_PAIR : FAM_SINGLE;
-  const bool packed = fam == FAM_REG;
+                     : c->lay == TPAIR_REG ? FAM_REG : c->lay == TSINGLE_REG ? FAM_REG1
+                     : c->lay == TPAIR ? FAM_PAIR : FAM_SINGLE;
+  const bool packed = fam == FAM_REG || fam == FAM_REG1;
   const int n = m + r - 1;
   const int per = per_cand(m, r);
   // floats per candidate in the params: Huffman = matrices + programs, mixed = fp64 matrices
@@ -293,7 +299,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
                              : sweep_max_cands_per_launch(dims, m, r);
   const int dy = dims == 1 ? m : m * m;
   const long long n_tblk = n_tiles <= 0 ? 0 : n_tblk_of(dims, fam, n_tiles);
-  const long long n_groups = n_tblk * (dims == 1 ? kKP1 : 1);   // packed tile groups (FAM_REG)
+  const long long n_groups = n_tblk * (dims == 1 ? kKP1 : 1);   // packed tile groups (register kernels)
   const int tpc = tblk_per_cta(std::max(n_tblk, 1LL));
   const int n_tg = (int)((n_tblk + tpc - 1) / tpc);
   const bool work = n_tiles > 0 && n_cand > 0;
@@ -304,6 +310,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     return set_error(WINO_E_WORKSPACE, "sweep workspace %zu < %zu bytes", ws_bytes, L.total);
   auto at = [&](size_t off) { return work ? ws + off : nullptr; };
   double* y64 = reinterpret_cast<double*>(at(L.y64));
+  double* y64t = reinterpret_cast<double*>(at(L.y64t));
   u64* dp = reinterpret_cast<u64*>(at(L.dp));
   u64* gp = reinterpret_cast<u64*>(at(L.gp));
   u64* yh = reinterpret_cast<u64*>(at(L.yh));
@@ -318,11 +325,10 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   } else if (mixed) {
     smem = (size_t)dy * kSwThreads * 8 + (size_t)kMaxCpc * 4 * kPartial * 8;
   } else if (packed) {
-    smem = (dims == 2 ? (size_t)dy * kSwThreads * 16 : 0) + kStatSmem;
+    smem = (dims == 2 ? (size_t)dy * kSwThreads * (fam == FAM_REG ? 16 : 8) : 0) + kStatSmem;
   } else {
     const int W = fam == FAM_PAIR ? 2 : 1;
-    smem = (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)dy * W * kSwThreads * 8 +
-           (size_t)kMaxCpc * 4 * kPartial * 8;
+    smem = (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)kMaxCpc * 4 * kPartial * 8;
   }
   if (work && smem > 48 * 1024) {
     std::vector<SweepKernel> ks;
@@ -411,13 +417,9 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
       } else {
         const int tpb = 256;
         const unsigned nb = (unsigned)((n_tiles + tpb - 1) / tpb);
-        const auto refs = find_cfg(dims, m, r)->refs ? find_cfg(dims, m, r)->refs : nullptr;
-        if (!refs) {
-          status = set_error(WINO_E_UNSUPPORTED, "no fp64 reference kernel for this layout");
-          break;
-        }
+        const auto refs = c->refs;
         timed_launch(dims == 1 ? "sweep_refs1d" : "sweep_refs2d", stream, [&] {
-          refs<<<nb, tpb, 0, stream>>>(d_tiles, g_tiles, y64, (long long)n_tiles, ref_part);
+          refs<<<nb, tpb, 0, stream>>>(d_tiles, g_tiles, y64, y64t, (long long)n_tiles, ref_part);
           sweep_refs_total_kernel<<<1, 32, 0, stream>>>(ref_part, (int)nb, ref_tot);
         });
       }
@@ -459,6 +461,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     args.d = d_tiles;
     args.g = g_tiles;
     args.y64 = y64;
+    args.y64t = y64t;
     args.dp = dp;
     args.gp = gp;
     args.yh = yh;

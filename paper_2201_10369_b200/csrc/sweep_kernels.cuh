@@ -31,7 +31,8 @@ struct IdxParam {
 struct SweepArgs {
   const float* d;      // raw tiles [n_tiles][n^dims] (generic kernels)
   const float* g;      // [n_tiles][r^dims]
-  const double* y64;   // [n_tiles][m^dims] fp64 references (generic kernels)
+  const double* y64;   // [n_tiles][m^dims] fp64 references (Huffman / mixed kernels)
+  const double* y64t;  // [n_tiles / 128][m^dims][128] the same, tile-block-major (generic 2D)
   const u64* dp;       // packed tile pairs (register kernels, K6 prep): [group][n^dims][128]
   const u64* gp;       // [group][r^dims][128]
   const u64* yh;       // [group][m^dims][128]  y64 = hi + lo as fp32 pairs
@@ -207,6 +208,32 @@ struct Stat32 {
   }
 };
 
+// single-tile counterpart of Stat32 (large-n register kernels, one tile per thread)
+struct Stat32S {
+  float s0 = 0.0f, s1 = 0.0f, m0 = 0.0f;
+  __device__ __forceinline__ void add(float y, float hi, float lo) {
+    const float e = __fsub_rn(__fsub_rn(y, hi), lo);
+    const float ae = fabsf(e);
+    s0 = __fadd_rn(s0, ae);
+    s1 = __fmaf_rn(e, e, s1);
+    m0 = fmaxf(m0, ae);
+  }
+  __device__ __forceinline__ void fold(float& v0, float& v1, float& vm) const {
+    v0 = s0;
+    v1 = s1;
+    vm = m0;
+  }
+};
+
+template <bool PAIR>
+struct StatF {
+  typedef Stat32 type;
+};
+template <>
+struct StatF<false> {
+  typedef Stat32S type;
+};
+
 // Shared-memory statistics of the register kernels: per (candidate of the work item, thread)
 // three fp32 accumulators [kMaxCpc][3][kSwThreads] (thread-private slots: no barrier, no
 // warp reduction inside the candidate loop) and a per-candidate "needs the careful path"
@@ -226,7 +253,8 @@ struct SmemStats {
   }
   // accumulate one (candidate, tile block) contribution of this thread; `first`: the work
   // item's first tile block (initialise instead of reading)
-  __device__ __forceinline__ void add(int k, bool first, const Stat32& st32) const {
+  template <class ST>
+  __device__ __forceinline__ void add(int k, bool first, const ST& st32) const {
     float* a = acc + k * 3 * kSwThreads + threadIdx.x;
     float o0 = 0.0f, o1 = 0.0f, o2 = 0.0f;
     if (!first) {
@@ -298,14 +326,19 @@ struct SmemStats {
 
 // ------------------------------------------------------------------ K6: fp64 references
 // Generic layouts: y64 [n_tiles][m^dims] = fp64 direct valid correlation of every tile
-// (c-independent, once per call) + per-block Σ|y64| / max|y64|.
+// (c-independent, once per call) + per-block Σ|y64| / max|y64|; y64t = the same values
+// tile-block-major [t / 128][m^dims][t % 128] (coalesced per-output reads of the generic 2D
+// kernel; padding tiles of the last blocks are 0).
 template <int DIMS, int M, int R>
 __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict__ d, const float* __restrict__ g,
-                                                         double* __restrict__ y64, long long n_tiles,
-                                                         double* __restrict__ ref_part) {
+                                                         double* __restrict__ y64, double* __restrict__ y64t,
+                                                         long long n_tiles, double* __restrict__ ref_part) {
   constexpr int N = M + R - 1;
   constexpr int DN = DIMS == 1 ? N : N * N, DG = DIMS == 1 ? R : R * R, DY = DIMS == 1 ? M : M * M;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double* yt_t = y64t + (t >> 7) * DY * kSwThreads + (t & (kSwThreads - 1));
+  if (t >= n_tiles)
+    for (int o = 0; o < DY; o++) yt_t[o * kSwThreads] = 0.0;
   double s = 0.0, mx = 0.0;
   if (t < n_tiles) {
     const float* dt = d + t * DN;
@@ -316,6 +349,7 @@ __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict
         double acc = 0.0;
         for (int j = 0; j < R; j++) acc = __dadd_rn(acc, __dmul_rn((double)gt[j], (double)dt[p + j]));
         yt[p] = acc;
+        yt_t[p * kSwThreads] = acc;
         s += fabs(acc);
         mx = fmax(mx, fabs(acc));
       }
@@ -327,6 +361,7 @@ __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict
             for (int v = 0; v < R; v++)
               acc = __dadd_rn(acc, __dmul_rn((double)gt[u * R + v], (double)dt[(p + u) * N + q + v]));
           yt[p * M + q] = acc;
+          yt_t[(p * M + q) * kSwThreads] = acc;
           s += fabs(acc);
           mx = fmax(mx, fabs(acc));
         }
@@ -356,11 +391,13 @@ __global__ void __launch_bounds__(256) sweep_refs_kernel(const float* __restrict
 }
 
 // Register layouts: the same fp64 references, plus the tiles and references repacked into
-// coalesced pairs.  Group G = tiles [256 G, 256 G + 256); element e of lane tid is the u64
-// (tile 256 G + tid, tile 256 G + 128 + tid); y64 is split into fp32 hi = RN32(y64) and
-// lo = RN32(y64 − hi).  Padding tiles (>= n_tiles) are zeros.  One CTA per group; per-CTA
-// Σ|y64|, max|y64| partials in the same fixed order for any candidate sharding.
-template <int DIMS, int M, int R>
+// coalesced per-lane layouts.  PAIR: group G = tiles [256 G, 256 G + 256); element e of
+// lane tid is the u64 (tile 256 G + tid, tile 256 G + 128 + tid).  Single: group G = tiles
+// [128 G, 128 G + 128), element e of lane tid is the float of tile 128 G + tid.  y64 is split
+// into fp32 hi = RN32(y64) and lo = RN32(y64 − hi).  Padding tiles (>= n_tiles) are zeros.
+// One CTA per group; per-CTA Σ|y64|, max|y64| partials in the same fixed order for any
+// candidate sharding.
+template <int DIMS, int M, int R, bool PAIR>
 __global__ void __launch_bounds__(kSwThreads) sweep_prep_kernel(const float* __restrict__ d,
                                                                 const float* __restrict__ g, long long n_tiles,
                                                                 u64* __restrict__ dp, u64* __restrict__ gp,
@@ -368,13 +405,14 @@ __global__ void __launch_bounds__(kSwThreads) sweep_prep_kernel(const float* __r
                                                                 double* __restrict__ ref_part) {
   constexpr int N = M + R - 1;
   constexpr int DN = DIMS == 1 ? N : N * N, DG = DIMS == 1 ? R : R * R, DY = DIMS == 1 ? M : M * M;
+  constexpr int W = PAIR ? 2 : 1;
   const long long grp = blockIdx.x;
   const int tid = threadIdx.x;
   double s = 0.0, mx = 0.0;
   float y_hi[2][DY], y_lo[2][DY];
 #pragma unroll 1
-  for (int h = 0; h < 2; h++) {
-    const long long t = grp * kGroupTiles + h * kSwThreads + tid;
+  for (int h = 0; h < W; h++) {
+    const long long t = grp * (W * kSwThreads) + h * kSwThreads + tid;
     const bool ok = t < n_tiles;
     const float* dt = d + t * DN;
     const float* gt = g + t * DG;
@@ -397,16 +435,30 @@ __global__ void __launch_bounds__(kSwThreads) sweep_prep_kernel(const float* __r
       y_lo[h][o] = __double2float_rn(acc - (double)y_hi[h][o]);
     }
   }
-  const long long t0 = grp * kGroupTiles + tid, t1 = t0 + kSwThreads;
-  const bool ok0 = t0 < n_tiles, ok1 = t1 < n_tiles;
-  for (int e = 0; e < DN; e++)
-    dp[(grp * DN + e) * kSwThreads + tid] = pack2(ok0 ? __ldg(d + t0 * DN + e) : 0.0f, ok1 ? __ldg(d + t1 * DN + e) : 0.0f);
-  for (int e = 0; e < DG; e++)
-    gp[(grp * DG + e) * kSwThreads + tid] = pack2(ok0 ? __ldg(g + t0 * DG + e) : 0.0f, ok1 ? __ldg(g + t1 * DG + e) : 0.0f);
+  const long long t0 = grp * (W * kSwThreads) + tid, t1 = t0 + kSwThreads;
+  const bool ok0 = t0 < n_tiles, ok1 = PAIR && t1 < n_tiles;
+  if constexpr (PAIR) {
+    for (int e = 0; e < DN; e++)
+      dp[(grp * DN + e) * kSwThreads + tid] = pack2(ok0 ? __ldg(d + t0 * DN + e) : 0.0f, ok1 ? __ldg(d + t1 * DN + e) : 0.0f);
+    for (int e = 0; e < DG; e++)
+      gp[(grp * DG + e) * kSwThreads + tid] = pack2(ok0 ? __ldg(g + t0 * DG + e) : 0.0f, ok1 ? __ldg(g + t1 * DG + e) : 0.0f);
 #pragma unroll
-  for (int o = 0; o < DY; o++) {
-    yh[(grp * DY + o) * kSwThreads + tid] = pack2(y_hi[0][o], y_hi[1][o]);
-    yl[(grp * DY + o) * kSwThreads + tid] = pack2(y_lo[0][o], y_lo[1][o]);
+    for (int o = 0; o < DY; o++) {
+      yh[(grp * DY + o) * kSwThreads + tid] = pack2(y_hi[0][o], y_hi[1][o]);
+      yl[(grp * DY + o) * kSwThreads + tid] = pack2(y_lo[0][o], y_lo[1][o]);
+    }
+  } else {
+    float* dpf = reinterpret_cast<float*>(dp);
+    float* gpf = reinterpret_cast<float*>(gp);
+    float* yhf = reinterpret_cast<float*>(yh);
+    float* ylf = reinterpret_cast<float*>(yl);
+    for (int e = 0; e < DN; e++) dpf[(grp * DN + e) * kSwThreads + tid] = ok0 ? __ldg(d + t0 * DN + e) : 0.0f;
+    for (int e = 0; e < DG; e++) gpf[(grp * DG + e) * kSwThreads + tid] = ok0 ? __ldg(g + t0 * DG + e) : 0.0f;
+#pragma unroll
+    for (int o = 0; o < DY; o++) {
+      yhf[(grp * DY + o) * kSwThreads + tid] = y_hi[0][o];
+      ylf[(grp * DY + o) * kSwThreads + tid] = y_lo[0][o];
+    }
   }
   __shared__ double red[2][4];
 #pragma unroll
@@ -436,7 +488,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_prep_kernel(const float* __r
 // per-output finiteness, padding tiles excluded) and, if yd != NULL, writes the outputs.
 template <int M, int R, bool PAIR, bool NOFMA, bool CAREFUL, int Z>
 __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typename Lane<PAIR, NOFMA>::T* sd,
-                                       typename Lane<PAIR, NOFMA>::T* st2, const double* sy,
+                                       typename Lane<PAIR, NOFMA>::T* st2, const double* const (&yt)[2],
                                        const typename Lane<PAIR, NOFMA>::T (&g)[R * R], int tid, Stat& st,
                                        float* yd, long long tile0, long long n_tiles) {
   using L = Lane<PAIR, NOFMA>;
@@ -511,22 +563,24 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       for (int h = 0; h < W; h++) {
         const bool ok = tile0 + tid + h * kSwThreads < n_tiles;
         if (yd != nullptr && ok) yd[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
+        const double yref = __ldg(yt[h] + o * kSwThreads);   // coalesced, L1/L2-resident
         if (CAREFUL) {
           if (ok) {
-            if (h == 0) st.template add_careful<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-            else st.template add_careful<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+            if (h == 0) st.template add_careful<0>(L::get(y, h), yref);
+            else st.template add_careful<1>(L::get(y, h), yref);
           }
         } else {
-          if (h == 0) st.template add_fast<0>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
-          else st.template add_fast<1>(L::get(y, h), sy[(o * W + h) * kSwThreads + tid]);
+          if (h == 0) st.template add_fast<0>(L::get(y, h), yref);
+          else st.template add_fast<1>(L::get(y, h), yref);
         }
       }
     }
   }
 }
 
-// smem: sd [NN][128] T (tiles), st2 [NN][128] T (T2 staging), sy [MM][W][128] double,
-//       sacc [kMaxCpc][4 warps][kPartial] double
+// smem: sd [NN][128] T (tiles), st2 [NN][128] T (T2 staging), sacc [kMaxCpc][4 warps][kPartial]
+// double; the fp64 references are read per output from y64t (no shared-memory copy: the
+// large-n tiles need the capacity for occupancy)
 template <int M, int R, bool PAIR, bool NOFMA, int Z>
 __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                              const __grid_constant__ IdxParam DI) {
@@ -540,8 +594,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
   extern __shared__ __align__(16) unsigned char smem[];
   T* sd = reinterpret_cast<T*>(smem);
   T* st2 = sd + NN * kSwThreads;
-  double* sy = reinterpret_cast<double*>(st2 + NN * kSwThreads);
-  double* sacc = sy + MM * W * kSwThreads;
+  double* sacc = reinterpret_cast<double*>(st2 + NN * kSwThreads);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // persistent CTAs walk the (candidate group, tile group) work items round-robin
@@ -595,21 +648,6 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
             else reinterpret_cast<float*>(sd)[e * kSwThreads + tid] = v[0];
           }
         }
-#pragma unroll
-        for (int h = 0; h < W; h++) {
-          const double* ysrc = a.y64 + (tile0 + tid + h * kSwThreads) * MM;
-          if constexpr (MM % 2 == 0) {
-#pragma unroll 4
-            for (int o2 = 0; o2 < MM / 2; o2++) {
-              const double2 v = ok[h] ? __ldg(reinterpret_cast<const double2*>(ysrc) + o2) : make_double2(0.0, 0.0);
-              sy[((2 * o2) * W + h) * kSwThreads + tid] = v.x;
-              sy[((2 * o2 + 1) * W + h) * kSwThreads + tid] = v.y;
-            }
-          } else {
-#pragma unroll 4
-            for (int o = 0; o < MM; o++) sy[(o * W + h) * kSwThreads + tid] = ok[h] ? __ldg(ysrc + o) : 0.0;
-          }
-        }
       }
       T g[RR];
 #pragma unroll
@@ -625,16 +663,22 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
       }
       __syncthreads();
 
+      const double* yt[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const long long t = tile0 + tid + (W == 2 ? h : 0) * kSwThreads;
+        yt[h] = a.y64t + (t >> 7) * MM * kSwThreads + (t & (kSwThreads - 1));
+      }
       for (int s = c_begin; s < c_end; s++) {
         const float* cm = P.v + s * PER;
         Stat st;
         float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
-        eval2d<M, R, PAIR, NOFMA, false, Z>(cm, sd, st2, sy, g, tid, st, yd, tile0, a.n_tiles);
+        eval2d<M, R, PAIR, NOFMA, false, Z>(cm, sd, st2, yt, g, tid, st, yd, tile0, a.n_tiles);
         if (__any_sync(0xffffffffu, !st.finite())) {
           // exact per-output path with the dense chains (the oracle's; a skipped zero term
           // can hide an inf * 0 = NaN of the dense chain), padding tiles excluded
           st = Stat();
-          eval2d<M, R, PAIR, NOFMA, true, 0>(cm, sd, st2, sy, g, tid, st, yd, tile0, a.n_tiles);
+          eval2d<M, R, PAIR, NOFMA, true, 0>(cm, sd, st2, yt, g, tid, st, yd, tile0, a.n_tiles);
         }
         st.warp_reduce();
         if (lane == 0) {
@@ -663,15 +707,21 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
 }
 
 // ------------------------------------------------------------------ K7 (2D, tiles in registers)
-// For small n: the thread's two tiles d stay in registers and T2 is formed row by row from
-// them (T2[i][q] = Σ_j Bᵀ[i][j] d[j][q], ascending j), so no candidate-dependent data
-// touches shared memory; only y64 (hi, lo pairs) is staged.  Same chains as eval2d.
-template <int M, int R, bool NOFMA, bool CAREFUL, int Z>
-__device__ __forceinline__ void eval2d_r(const float* __restrict__ cm, const u64 (&d)[(M + R - 1) * (M + R - 1)],
-                                         const u64 (&g)[R * R], const u64* syh, const u64* syl, int tid, Stat& st,
-                                         Stat32& st32, float* yd, long long tile0, long long n_tiles) {
-  using L = Lane<true, NOFMA>;
-  using T = u64;
+// For small n (PAIR: the thread's two tiles) or large n (single: one tile): the tiles d stay
+// in registers and T2 is formed row by row from them (T2[i][q] = Σ_j Bᵀ[i][j] d[j][q],
+// ascending j), so no candidate-dependent data touches shared memory; only y64 (hi, lo) is
+// staged.  Same chains as eval2d.
+template <int M, int R, bool PAIR, bool NOFMA, bool CAREFUL, int Z>
+__device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
+                                         const typename Lane<PAIR, NOFMA>::T (&d)[(M + R - 1) * (M + R - 1)],
+                                         const typename Lane<PAIR, NOFMA>::T (&g)[R * R],
+                                         const typename Lane<PAIR, NOFMA>::T* syh,
+                                         const typename Lane<PAIR, NOFMA>::T* syl, int tid, Stat& st,
+                                         typename StatF<PAIR>::type& st32, float* yd, long long tile0,
+                                         long long n_tiles) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
+  constexpr int W = L::W;
   constexpr int N = M + R - 1, MM = M * M;
   constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
   T t3[M][N];
@@ -726,16 +776,16 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm, const u64
       const int o = p * M + q;
       if (yd != nullptr) {
 #pragma unroll
-        for (int h = 0; h < 2; h++)
+        for (int h = 0; h < W; h++)
           if (tile0 + tid + h * kSwThreads < n_tiles) yd[(tid + h * kSwThreads) * MM + o] = L::get(y, h);
       }
       if (CAREFUL) {
         // exact fp64 path on y64 = hi + lo (the split is exact in fp64 to 2^-48 relative)
-        float h0, h1, l0, l1;
-        split2(syh[o * kSwThreads + tid], h0, h1);
-        split2(syl[o * kSwThreads + tid], l0, l1);
-        if (tile0 + tid < n_tiles) st.template add_careful<0>(L::get(y, 0), (double)h0 + (double)l0);
-        if (tile0 + tid + kSwThreads < n_tiles) st.template add_careful<1>(L::get(y, 1), (double)h1 + (double)l1);
+        const T hp = syh[o * kSwThreads + tid], lp = syl[o * kSwThreads + tid];
+        if (tile0 + tid < n_tiles)
+          st.template add_careful<0>(L::get(y, 0), (double)L::get(hp, 0) + (double)L::get(lp, 0));
+        if (W == 2 && tile0 + tid + kSwThreads < n_tiles)
+          st.template add_careful<1>(L::get(y, 1), (double)L::get(hp, 1) + (double)L::get(lp, 1));
       } else {
         st32.add(y, syh[o * kSwThreads + tid], syl[o * kSwThreads + tid]);
       }
@@ -743,25 +793,32 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm, const u64
   }
 }
 
-// Coalesced loads of the thread's packed tile pair (group grp).
-template <int NN, int RR>
-__device__ __forceinline__ void load_pair2d(const SweepArgs& a, long long grp, int tid, u64 (&d)[NN], u64 (&g)[RR]) {
+// Coalesced loads of the thread's packed tile(s) (group grp).
+template <class T, int NN, int RR>
+__device__ __forceinline__ void load_tiles2d(const SweepArgs& a, long long grp, int tid, T (&d)[NN], T (&g)[RR]) {
+  const T* dp = reinterpret_cast<const T*>(a.dp);
+  const T* gp = reinterpret_cast<const T*>(a.gp);
 #pragma unroll
-  for (int e = 0; e < NN; e++) d[e] = __ldg(a.dp + (grp * NN + e) * kSwThreads + tid);
+  for (int e = 0; e < NN; e++) d[e] = __ldg(dp + (grp * NN + e) * kSwThreads + tid);
 #pragma unroll
-  for (int e = 0; e < RR; e++) g[e] = __ldg(a.gp + (grp * RR + e) * kSwThreads + tid);
+  for (int e = 0; e < RR; e++) g[e] = __ldg(gp + (grp * RR + e) * kSwThreads + tid);
 }
 
-// smem: syh [MM][128] u64, syl [MM][128] u64, then SmemStats
-template <int M, int R, bool NOFMA, int Z>
+// smem: syh [MM][128] T, syl [MM][128] T, then SmemStats
+template <int M, int R, bool PAIR, bool NOFMA, int Z>
 __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                                  const __grid_constant__ IdxParam DI) {
+  using L = Lane<PAIR, NOFMA>;
+  using T = typename L::T;
   constexpr int N = M + R - 1, NN = N * N, MM = M * M, RR = R * R;
   constexpr int PER = M * N + N * R + N * N;
+  constexpr int TPB = L::W * kSwThreads;
   extern __shared__ __align__(16) unsigned char smem[];
-  u64* syh = reinterpret_cast<u64*>(smem);            // [MM][128] (hi_A, hi_B)
-  u64* syl = syh + MM * kSwThreads;                    // [MM][128] (lo_A, lo_B)
+  T* syh = reinterpret_cast<T*>(smem);            // [MM][128] (hi_A, hi_B) / hi
+  T* syl = syh + MM * kSwThreads;                  // [MM][128] (lo_A, lo_B) / lo
   const SmemStats ss = SmemStats::at(reinterpret_cast<unsigned char*>(syl + MM * kSwThreads));
+  const T* gyh = reinterpret_cast<const T*>(a.yh);
+  const T* gyl = reinterpret_cast<const T*>(a.yl);
 
   const int tid = threadIdx.x;
   const int n_items = a.n_cgroups * a.n_tgroups;
@@ -776,21 +833,21 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
     if (tid < kMaxCpc) ss.flag[tid] = 0;
     __syncthreads();
     for (int tb = tb_begin; tb < tb_end; tb++) {
-      const long long tile0 = (long long)tb * kGroupTiles;
-      u64 d[NN], g[RR];
-      load_pair2d<NN, RR>(a, tb, tid, d, g);
+      const long long tile0 = (long long)tb * TPB;
+      T d[NN], g[RR];
+      load_tiles2d<T, NN, RR>(a, tb, tid, d, g);
       // each thread stages (and later reads) only its own y64 slots: no barrier needed
 #pragma unroll 4
       for (int o = 0; o < MM; o++) {
-        syh[o * kSwThreads + tid] = __ldg(a.yh + ((long long)tb * MM + o) * kSwThreads + tid);
-        syl[o * kSwThreads + tid] = __ldg(a.yl + ((long long)tb * MM + o) * kSwThreads + tid);
+        syh[o * kSwThreads + tid] = __ldg(gyh + ((long long)tb * MM + o) * kSwThreads + tid);
+        syl[o * kSwThreads + tid] = __ldg(gyl + ((long long)tb * MM + o) * kSwThreads + tid);
       }
       for (int s = c_begin; s < c_end; s++) {
         const float* cm = P.v + s * PER;
         Stat st;
-        Stat32 st32;
+        typename StatF<PAIR>::type st32;
         float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
-        eval2d_r<M, R, NOFMA, false, Z>(cm, d, g, syh, syl, tid, st, st32, yd, tile0, a.n_tiles);
+        eval2d_r<M, R, PAIR, NOFMA, false, Z>(cm, d, g, syh, syl, tid, st, st32, yd, tile0, a.n_tiles);
         ss.add(s - c_begin, tb == tb_begin, st32);
       }
     }
@@ -803,14 +860,15 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
       const int s = c_begin + k;
       const float* cm = P.v + s * PER;
       Stat st;
-      Stat32 st32;
+      typename StatF<PAIR>::type st32;
       for (int tb = tb_begin; tb < tb_end; tb++) {
-        const long long tile0 = (long long)tb * kGroupTiles;
-        u64 d[NN], g[RR];
-        load_pair2d<NN, RR>(a, tb, tid, d, g);
+        const long long tile0 = (long long)tb * TPB;
+        T d[NN], g[RR];
+        load_tiles2d<T, NN, RR>(a, tb, tid, d, g);
         float* yd = a.ydump ? a.ydump + ((long long)DI.idx[s] * a.n_tiles + tile0) * MM : nullptr;
-        eval2d_r<M, R, NOFMA, true, 0>(cm, d, g, a.yh + (long long)tb * MM * kSwThreads,
-                                       a.yl + (long long)tb * MM * kSwThreads, tid, st, st32, yd, tile0, a.n_tiles);
+        eval2d_r<M, R, PAIR, NOFMA, true, 0>(cm, d, g, gyh + (long long)tb * MM * kSwThreads,
+                                             gyl + (long long)tb * MM * kSwThreads, tid, st, st32, yd, tile0,
+                                             a.n_tiles);
       }
       ss.write_careful(st, a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial);
     }
@@ -943,14 +1001,15 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
 }
 
 typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);
-typedef void (*RefsKernel)(const float*, const float*, double*, long long, double*);
+typedef void (*RefsKernel)(const float*, const float*, double*, double*, long long, double*);
 typedef void (*PrepKernel)(const float*, const float*, long long, u64*, u64*, u64*, u64*, double*);
 
 // Kernel layouts: TPAIR = two tiles per thread (FFMA2 lanes = tiles, coefficients per
 // candidate as uniform registers), tiles in shared memory; TSINGLE = one tile per thread
 // (FFMA), for large n; TPAIR_REG = tile pairs held in registers, packed inputs (K6 prep):
-// the 2D small-n kernel and every 1D kernel.
-enum Layout { TPAIR = 0, TSINGLE = 1, TPAIR_REG = 2 };
+// the 2D small-n kernels and every 1D kernel; TSINGLE_REG = one tile per thread held in
+// registers (2D large n).
+enum Layout { TPAIR = 0, TSINGLE = 1, TPAIR_REG = 2, TSINGLE_REG = 3 };
 
 struct Variant {
   int z;                         // structural-zero family (zero_masks.h; 0 = dense)
@@ -962,8 +1021,8 @@ struct Variant {
 struct SweepCfg {
   int dims, m, r;
   Layout lay;
-  RefsKernel refs;               // generic layouts
-  PrepKernel prep;               // TPAIR_REG
+  RefsKernel refs;               // generic layouts, Huffman, mixed
+  PrepKernel prep;               // TPAIR_REG, TSINGLE_REG
   std::vector<Variant> variants; // most specialised first, dense last
 };
 
@@ -981,9 +1040,10 @@ Variant make_variant() {
     static_assert(LAY == TPAIR_REG, "1D kernels are register-resident");
     v.k[0] = (SweepKernel)sweep1d_kernel<M, R, false, Z>;
     v.k[1] = (SweepKernel)sweep1d_kernel<M, R, true, Z>;
-  } else if constexpr (LAY == TPAIR_REG) {
-    v.k[0] = (SweepKernel)sweep2d_reg_kernel<M, R, false, Z>;
-    v.k[1] = (SweepKernel)sweep2d_reg_kernel<M, R, true, Z>;
+  } else if constexpr (LAY == TPAIR_REG || LAY == TSINGLE_REG) {
+    constexpr bool PAIR = LAY == TPAIR_REG;
+    v.k[0] = (SweepKernel)sweep2d_reg_kernel<M, R, PAIR, false, Z>;
+    v.k[1] = (SweepKernel)sweep2d_reg_kernel<M, R, PAIR, true, Z>;
   } else {
     constexpr bool PAIR = LAY == TPAIR;
     v.k[0] = (SweepKernel)sweep2d_kernel<M, R, PAIR, false, Z>;
@@ -1002,8 +1062,9 @@ SweepCfg make_cfg(std::vector<Variant> specialised = {}) {
   c.lay = LAY;
   c.refs = nullptr;
   c.prep = nullptr;
-  if constexpr (LAY == TPAIR_REG) c.prep = sweep_prep_kernel<DIMS, M, R>;
-  else c.refs = sweep_refs_kernel<DIMS, M, R>;
+  // refs: the generic layouts and the Huffman / mixed-precision kernels of every shape
+  c.refs = sweep_refs_kernel<DIMS, M, R>;
+  if constexpr (LAY == TPAIR_REG || LAY == TSINGLE_REG) c.prep = sweep_prep_kernel<DIMS, M, R, LAY == TPAIR_REG>;
   c.variants = specialised;
   c.variants.push_back(make_variant<DIMS, M, R, LAY, 0>());
   return c;
@@ -1022,6 +1083,7 @@ std::vector<SweepCfg> sweep_cfgs_1d_large();
 std::vector<SweepCfg> sweep_cfgs_2d_f43();
 std::vector<SweepCfg> sweep_cfgs_2d_small();
 std::vector<SweepCfg> sweep_cfgs_2d_large();
+std::vector<SweepCfg> sweep_cfgs_2d_mid();
 std::vector<HuffCfg> sweep_huff_cfgs();
 std::vector<HuffCfg> sweep_mixed_cfgs();
 
