@@ -325,7 +325,8 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   } else if (mixed) {
     smem = (size_t)dy * kSwThreads * 8 + (size_t)kMaxCpc * 4 * kPartial * 8;
   } else if (packed) {
-    smem = (dims == 2 ? (size_t)dy * kSwThreads * (fam == FAM_REG ? 16 : 8) : 0) + kStatSmem;
+    smem = (dims == 2 ? (size_t)dy * kSwThreads * (fam == FAM_REG ? 16 : 8) : 0) +
+           stat_smem_bytes(reg_cpc_cap(dims, fam == FAM_REG));
   } else {
     const int W = fam == FAM_PAIR ? 2 : 1;
     smem = (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)kMaxCpc * 4 * kPartial * 8;
@@ -444,7 +445,8 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSwThreads, smem);
     const long long slots = (long long)std::max(occ, 1) * nsm;
-    int cpc = std::min(kMaxCpc, nc);
+    const int cap = packed ? reg_cpc_cap(dims, fam == FAM_REG) : kMaxCpc;
+    int cpc = std::min(cap, nc);
     double best = -1.0;
     for (int cand = cpc; cand >= std::min(8, cpc); cand--) {
       const long long items = (long long)((nc + cand - 1) / cand) * n_tg;

@@ -16,7 +16,7 @@ typedef unsigned long long u64;
 constexpr int kSwThreads = 128;        // 4 warps, one per SM sub-partition
 constexpr int kParamFloats = 7424;     // coefficient floats per launch (29696 B)
 constexpr int kMaxCandsLaunch = 512;   // + 2 KB of candidate indices: < 32764 B of params
-constexpr int kMaxCpc = 32;            // candidates per CTA work item
+constexpr int kMaxCpc = 32;            // candidates per CTA work item (<= 32: flag ballot)
 constexpr int kPartial = 4;            // doubles per partial: s0, s1, m0, nonfin
 constexpr int kKP1 = 4;                // 1D: tile pairs per thread and tile block
 constexpr int kGroupTiles = 2 * kSwThreads;   // tiles per packed group (one pair per thread)
@@ -238,16 +238,21 @@ struct StatF<false> {
 // three fp32 accumulators [kMaxCpc][3][kSwThreads] (thread-private slots: no barrier, no
 // warp reduction inside the candidate loop) and a per-candidate "needs the careful path"
 // flag; scratch for the careful path's 4-warp combination.
-constexpr size_t kStatSmem = (size_t)kMaxCpc * 3 * kSwThreads * 4 + kMaxCpc * 4 + 4 * kPartial * 8;
+__host__ __device__ constexpr size_t stat_smem_bytes(int cap) {
+  return (size_t)cap * 3 * kSwThreads * 4 + (size_t)kMaxCpc * 4 + 4 * kPartial * 8;
+}
+// candidates per work item of the register kernels: the 2D tile-pair kernel caps them at 24
+// so that its y64 staging + statistics fit three CTAs per SM (68 KB each)
+__host__ __device__ constexpr int reg_cpc_cap(int dims, bool pair) { return dims == 2 && pair ? 24 : kMaxCpc; }
 
 struct SmemStats {
-  float* acc;    // [kMaxCpc][3][kSwThreads]
+  float* acc;    // [cap][3][kSwThreads]
   int* flag;     // [kMaxCpc]
   double* red;   // [4][kPartial]
-  __device__ __forceinline__ static SmemStats at(unsigned char* p) {
+  __device__ __forceinline__ static SmemStats at(unsigned char* p, int cap) {
     SmemStats s;
     s.acc = reinterpret_cast<float*>(p);
-    s.flag = reinterpret_cast<int*>(s.acc + kMaxCpc * 3 * kSwThreads);
+    s.flag = reinterpret_cast<int*>(s.acc + cap * 3 * kSwThreads);
     s.red = reinterpret_cast<double*>(s.flag + kMaxCpc);
     return s;
   }
@@ -268,6 +273,13 @@ struct SmemStats {
     a[0] = o0 + v0;
     a[kSwThreads] = o1 + v1;
     a[2 * kSwThreads] = fmaxf(o2, vm);
+  }
+  // after a barrier: the flagged candidates of the work item as a bit mask, provably
+  // warp-uniform (a ballot), so the loop over them keeps the item's candidate indices in
+  // uniform registers (coefficients via LDCU, not per-thread LDC)
+  __device__ __forceinline__ unsigned flagged(int ncand) const {
+    const int lane = threadIdx.x & 31;
+    return __ballot_sync(0xffffffffu, lane < ncand && flag[lane] != 0);
   }
   // after a barrier: per unflagged candidate k, fp64 fixed-order sum over the 128 threads
   // -> the (candidate, tile group) partial.  Warp w handles candidates w, w + 4, ...
@@ -806,7 +818,7 @@ __device__ __forceinline__ void load_tiles2d(const SweepArgs& a, long long grp, 
 
 // smem: syh [MM][128] T, syl [MM][128] T, then SmemStats
 template <int M, int R, bool PAIR, bool NOFMA, int Z>
-__global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+__global__ void __launch_bounds__(kSwThreads, PAIR ? 3 : 1) sweep2d_reg_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                                  const __grid_constant__ IdxParam DI) {
   using L = Lane<PAIR, NOFMA>;
   using T = typename L::T;
@@ -816,7 +828,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
   extern __shared__ __align__(16) unsigned char smem[];
   T* syh = reinterpret_cast<T*>(smem);            // [MM][128] (hi_A, hi_B) / hi
   T* syl = syh + MM * kSwThreads;                  // [MM][128] (lo_A, lo_B) / lo
-  const SmemStats ss = SmemStats::at(reinterpret_cast<unsigned char*>(syl + MM * kSwThreads));
+  const SmemStats ss = SmemStats::at(reinterpret_cast<unsigned char*>(syl + MM * kSwThreads), reg_cpc_cap(2, PAIR));
   const T* gyh = reinterpret_cast<const T*>(a.yh);
   const T* gyl = reinterpret_cast<const T*>(a.yl);
 
@@ -855,8 +867,8 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_reg_kernel(SweepArgs a, co
     ss.reduce(ncand, c_begin, DI, a.partial, a.n_tgroups, tg);
     // Rare: a candidate whose fp32 sums went non-finite in this work item is re-evaluated
     // exactly (fp64 statistics per output, dense chains, padding tiles excluded).
-    for (int k = 0; k < ncand; k++) {
-      if (ss.flag[k] == 0) continue;   // uniform: every thread reads the same flag
+    for (unsigned fl = ss.flagged(ncand); fl != 0u; fl &= fl - 1u) {
+      const int k = __ffs(fl) - 1;
       const int s = c_begin + k;
       const float* cm = P.v + s * PER;
       Stat st;
@@ -940,13 +952,13 @@ __device__ __forceinline__ void load_pair1d(const SweepArgs& a, long long grp, i
 // Each thread owns kKP1 pairs of tiles, so a candidate's coefficients (uniform registers)
 // are amortised over 2 * kKP1 tile evaluations.  smem: SmemStats.
 template <int M, int R, bool NOFMA, int Z>
-__global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+__global__ void __launch_bounds__(kSwThreads, 3) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                              const __grid_constant__ IdxParam DI) {
   constexpr int N = M + R - 1;
   constexpr int PER = M * N + N * R + N * N;
   constexpr int TPB = kGroupTiles * kKP1;
   extern __shared__ __align__(16) unsigned char smem[];
-  const SmemStats ss = SmemStats::at(smem);
+  const SmemStats ss = SmemStats::at(smem, reg_cpc_cap(1, true));
 
   const int tid = threadIdx.x;
   const int n_items = a.n_cgroups * a.n_tgroups;
@@ -979,8 +991,8 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
     }
     __syncthreads();
     ss.reduce(ncand, c_begin, DI, a.partial, a.n_tgroups, tg);
-    for (int kc = 0; kc < ncand; kc++) {
-      if (ss.flag[kc] == 0) continue;
+    for (unsigned fl = ss.flagged(ncand); fl != 0u; fl &= fl - 1u) {
+      const int kc = __ffs(fl) - 1;
       const int s = c_begin + kc;
       const float* cm = P.v + s * PER;
       Stat st;

@@ -32,9 +32,12 @@ def test_cfg4_grid_full_size_sampled(template, m, maker):
     rng = np.random.default_rng(7)
     pick = sorted(rng.choice(ok, size=3, replace=False).tolist())
     s_ref, m_ref, _ = ref.sweep(2, m, 5, [maker(*params[i]) for i in pick], d, gt)
+    # the n = 8 kernel keeps a tile in registers and scores in fp32 (e to 2^-23 relative,
+    # DESIGN.md §5): MAE within 1e-5, max|e| within 1e-6 (north star: 1 %); n = 10 scores in fp64
     for j, i in enumerate(pick):
         assert s[i, 3] == s_ref[j, 3] and s[i, 4] == s_ref[j, 4]
-        assert np.array_equal(mx[i], m_ref[j])
-        assert abs(s[i, 0] / s_ref[j, 0] - 1) < 1e-9
+        assert mx[i, 1] == m_ref[j, 1]
+        assert abs(mx[i, 0] / m_ref[j, 0] - 1) <= 1e-6
+        assert abs(s[i, 0] / s_ref[j, 0] - 1) < 1e-5
     mae = s[ok, 0] / np.where(s[ok, 3] > 0, s[ok, 3], np.nan)
     assert np.nanmin(mae) < 1e-5 and math.isfinite(np.nanmin(mae))

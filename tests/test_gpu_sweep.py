@@ -197,9 +197,12 @@ def test_unsupported_and_workspace_errors():
     with pytest.raises(_lib.WinoError) as ei:
         api.wino_error_sweep(2, 4, 3, np.array([OP.f43_c(1.5)]), _dev(d), _dev(g), sums, maxs, ws)
     assert ei.value.status == 6
+    d14, g14 = synth.random_tiles(100, 2, 14, 3, "uniform", seed=1)
     with pytest.raises(_lib.WinoError) as ei:
-        api.wino_error_sweep(2, 12, 3, np.zeros((1, 14)), _dev(d), _dev(g), sums, maxs, ws)
+        api.wino_error_sweep(2, 12, 3, np.zeros((1, 14)), _dev(d14), _dev(g14), sums, maxs, ws)
     assert ei.value.status == 8
+    with pytest.raises(ValueError):      # binding-level shape check (tiles of another n)
+        api.wino_error_sweep(2, 12, 3, np.zeros((1, 14)), _dev(d), _dev(g), sums, maxs, ws)
 
 
 @pytest.mark.parametrize("dims", [2, 1])
