@@ -950,9 +950,12 @@ __device__ __forceinline__ void load_pair1d(const SweepArgs& a, long long grp, i
 
 // Everything in registers; a CTA walks its tile blocks and, per block, its candidates.
 // Each thread owns kKP1 pairs of tiles, so a candidate's coefficients (uniform registers)
-// are amortised over 2 * kKP1 tile evaluations.  smem: SmemStats.
+// are amortised over 2 * kKP1 tile evaluations.  smem: SmemStats.  No min-blocks launch
+// bound: capping the registers (2-3 CTAs/SM) made ptxas move the coefficients from uniform
+// registers (LDCU) to per-thread LDC loads and re-load the tiles per candidate (measured
+// 1.7x slower).
 template <int M, int R, bool NOFMA, int Z>
-__global__ void __launch_bounds__(kSwThreads, 3) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
+__global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const __grid_constant__ MatsParam P,
                                                              const __grid_constant__ IdxParam DI) {
   constexpr int N = M + R - 1;
   constexpr int PER = M * N + N * R + N * N;
