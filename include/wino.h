@@ -140,6 +140,20 @@ int wino_conv2d_fp32_ex(const float* x, const float* w, float* y,
                         const double* points, void* workspace, size_t workspace_bytes,
                         double* d_sums, double* d_maxs, unsigned flags, void* stream);
 
+/* (2d) The layer with the network glue of configs[4] fused into its output transform:
+ *   act = maxpool_pool(ReLU(conv)), pool 1 | 2 (2 x 2 window, stride 2, floor), DEVICE
+ *   float[N][K][Ho/pool][Wo/pool]; y: DEVICE float[N][K][Ho][Wo] conv output, or NULL when
+ *   neither the scoring (d_sums) nor the caller needs it (then y is never materialised).
+ *   For even m the ReLU / pool run in the output-transform epilogue (a pooling window never
+ *   straddles two m x m tiles); odd m with pool 2 needs y and runs kernel (2b) after it.
+ *   ReLU and max are exact: act equals wino_relu_pool_fp32(y) bit for bit.  Other arguments,
+ *   flags and errors as (2c); INVALID_ARG also for act == NULL, pool not 1|2, or y == NULL
+ *   where it is required. */
+int wino_conv2d_relu_pool_fp32(const float* x, const float* w, float* y, float* act,
+                               int N, int C, int H, int W, int K, int r, int pad, int m,
+                               const double* points, void* workspace, size_t workspace_bytes,
+                               double* d_sums, double* d_maxs, int pool, unsigned flags, void* stream);
+
 /* (2b) Network glue for BASELINE.json configs[4] (VGG-16 "ReLU + 2x2 maxpool"):
  *   y[n][c][h][w] = max(0, max_{a,b < pool} x[n][c][pool h + a][pool w + b]), pool 1 | 2
  *   (2 x 2 window, stride 2, floor).  x: DEVICE float[N][C][H][W], y: DEVICE

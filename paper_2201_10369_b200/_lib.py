@@ -30,6 +30,8 @@ SIGNATURES = [
     ("wino_conv2d_fp32_ex", ctypes.c_int,
      [_vp, _vp, _vp] + [ctypes.c_int] * 8 + [_d, _vp, _sz, _vp, _vp, ctypes.c_uint, _vp]),
     ("wino_relu_pool_fp32", ctypes.c_int, [_vp, _vp] + [ctypes.c_int] * 5 + [_vp]),
+    ("wino_conv2d_relu_pool_fp32", ctypes.c_int,
+     [_vp, _vp, _vp, _vp] + [ctypes.c_int] * 8 + [_d, _vp, _sz, _vp, _vp, ctypes.c_int, ctypes.c_uint, _vp]),
     ("wino_error_sweep_workspace_bytes", _sz, [ctypes.c_int] * 4 + [_i64]),
     ("wino_error_sweep", ctypes.c_int,
      [ctypes.c_int] * 3 + [_d, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _i, _vp, _sz, ctypes.c_uint, _vp]),

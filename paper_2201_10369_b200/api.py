@@ -102,6 +102,37 @@ def wino_conv2d_fp32(x, w, y, pad: int, m: int, points: Sequence[float], workspa
         check(st, "wino_conv2d_fp32")
 
 
+def wino_conv2d_relu_pool_fp32(x, w, y, act, pad: int, m: int, points: Sequence[float], workspace, pool: int,
+                               d_sums=None, d_maxs=None, stream=None, flags: int = 0) -> None:
+    """The layer with ReLU (+ 2x2 max pool) fused: act [N,K,Ho/pool,Wo/pool] fp32 CUDA tensor;
+    y [N,K,Ho,Wo] or None (required when scoring)."""
+    import torch
+    N, C, H, W = x.shape
+    K, C2, r, r2 = w.shape
+    if C2 != C or r2 != r:
+        raise ValueError("weight shape mismatch")
+    Ho, Wo = H + 2 * pad - r + 1, W + 2 * pad - r + 1
+    _check_tensor("x", x, torch.float32, (N, C, H, W))
+    _check_tensor("w", w, torch.float32, (K, C, r, r))
+    if y is not None:
+        _check_tensor("y", y, torch.float32, (N, K, Ho, Wo))
+    _check_tensor("act", act, torch.float32, (N, K, Ho // pool, Wo // pool))
+    if (d_sums is None) != (d_maxs is None):
+        raise ValueError("d_sums and d_maxs: both or neither")
+    if d_sums is not None:
+        rows = (N,) if flags & WINO_CONV_SCORE_PER_IMAGE else ()
+        _check_tensor("d_sums", d_sums, torch.float64, rows + (WINO_SUMS,))
+        _check_tensor("d_maxs", d_maxs, torch.float64, rows + (WINO_MAXS,))
+    pts = _np64(points)
+    if pts.shape != (m + r - 1,):
+        raise ValueError(f"points: expected {m + r - 1} values, got {pts.shape}")
+    st = load().wino_conv2d_relu_pool_fp32(_ptr(x), _ptr(w), _ptr(y), _ptr(act), N, C, H, W, K, r, pad, m,
+                                          pts.ctypes.data_as(_d), _ptr(workspace),
+                                          workspace.numel() * workspace.element_size(), _ptr(d_sums), _ptr(d_maxs),
+                                          pool, flags, _stream_ptr(stream))
+    check(st, "wino_conv2d_relu_pool_fp32")
+
+
 def wino_relu_pool_fp32(x, y, pool: int, stream=None) -> None:
     """y = maxpool_pool(ReLU(x)); x [N,C,H,W], y [N,C,H/pool,W/pool] fp32 CUDA tensors."""
     import torch

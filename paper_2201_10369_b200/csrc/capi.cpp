@@ -152,18 +152,23 @@ int wino_conv2d_fp32(const float* x, const float* w, float* y, int N, int C, int
                              0u, stream);
 }
 
-int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
-                        int m, const double* points, void* workspace, size_t workspace_bytes, double* d_sums,
-                        double* d_maxs, unsigned flags, void* stream) {
+static int conv_common(const float* x, const float* w, float* y, float* act, int pool, int N, int C, int H, int W,
+                       int K, int r, int pad, int m, const double* points, void* workspace, size_t workspace_bytes,
+                       double* d_sums, double* d_maxs, unsigned flags, void* stream) {
   reset_launches();
-  if (!x || !w || !y || !points) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  if (!x || !w || !points || (!y && !act)) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (N < 0 || C < 1 || H < 1 || W < 1 || K < 0 || r < 1 || m < 1 || pad < 0)
     return set_error(WINO_E_INVALID_ARG, "negative batch / output channels, non-positive size or negative pad");
   if (flags & ~(WINO_CONV_TF32 | WINO_CONV_3XTF32 | WINO_CONV_SCORE_PER_IMAGE))
     return set_error(WINO_E_INVALID_ARG, "unknown flags");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
+  if (act && pool != 1 && pool != 2) return set_error(WINO_E_INVALID_ARG, "pool must be 1 or 2");
+  if (!y && (d_sums || (act && pool == 2 && m % 2 != 0)))
+    return set_error(WINO_E_INVALID_ARG, "y is required for scoring and for pool 2 with odd m");
   if (H + 2 * pad < r || W + 2 * pad < r) return set_error(WINO_E_BAD_SHAPE, "empty output");
+  if (act && pool == 2 && (H + 2 * pad - r + 1 < 2 || W + 2 * pad - r + 1 < 2))
+    return set_error(WINO_E_BAD_SHAPE, "pool 2 needs an output of at least 2 x 2");
   const int n = m + r - 1;
   if (n > WINO_MAX_N) return set_error(WINO_E_UNSUPPORTED, "n > WINO_MAX_N");
   if (!layer_supported(m, r)) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
@@ -176,7 +181,30 @@ int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, 
   to_f32(G.data(), n * r, Gf.data());
   to_f32(BT.data(), n * n, BTf.data());
   return finish(layer_launch(x, w, y, N, C, H, W, K, r, pad, m, ATf.data(), Gf.data(), BTf.data(), workspace,
-                             workspace_bytes, d_sums, d_maxs, flags, (cudaStream_t)stream));
+                             workspace_bytes, d_sums, d_maxs, flags, (cudaStream_t)stream, act, act ? pool : 0));
+}
+
+int wino_conv2d_fp32_ex(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
+                        int m, const double* points, void* workspace, size_t workspace_bytes, double* d_sums,
+                        double* d_maxs, unsigned flags, void* stream) {
+  if (!y) {
+    reset_launches();
+    return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  }
+  return conv_common(x, w, y, nullptr, 0, N, C, H, W, K, r, pad, m, points, workspace, workspace_bytes, d_sums,
+                     d_maxs, flags, stream);
+}
+
+int wino_conv2d_relu_pool_fp32(const float* x, const float* w, float* y, float* act, int N, int C, int H, int W,
+                               int K, int r, int pad, int m, const double* points, void* workspace,
+                               size_t workspace_bytes, double* d_sums, double* d_maxs, int pool, unsigned flags,
+                               void* stream) {
+  if (!act) {
+    reset_launches();
+    return set_error(WINO_E_INVALID_ARG, "NULL act");
+  }
+  return conv_common(x, w, y, act, pool, N, C, H, W, K, r, pad, m, points, workspace, workspace_bytes, d_sums,
+                     d_maxs, flags, stream);
 }
 
 int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, int pool, void* stream) {

@@ -293,10 +293,17 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
 using tc::gemm_tf32_kernel;
 
 // ------------------------------------------------------------------ K4
-// one thread per (k, t); t fastest -> coalesced M loads per Winograd position
+// one thread per (k, t); t fastest -> coalesced M loads per Winograd position.
+// Epilogue (network glue of configs[4], fused): with act != NULL the thread also writes
+// act = maxpool_pool(ReLU(y)) of its tile (pool 1: ReLU; pool 2: 2 x 2 / 2 max pool, which
+// needs an even tile size so no window straddles two tiles -- the launcher only fuses then);
+// y itself is written only when y != NULL (the scorer and the caller's `keep` need it).
+// ReLU and max are exact, so the fused output equals relu_pool(y) bit for bit.
 template <int M, int R>
-__global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(const float* __restrict__ Mw, float* __restrict__ y, Geo geo,
-                                                        const __grid_constant__ LayerMats mt) {
+__global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(const float* __restrict__ Mw,
+                                                                           float* __restrict__ y, Geo geo,
+                                                                           const __grid_constant__ LayerMats mt,
+                                                                           float* __restrict__ act, int pool) {
   constexpr int N = M + R - 1;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * T
   if (idx >= (long long)geo.K * geo.T) return;
@@ -325,11 +332,15 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
   const int img = (int)(t / per_img);
   const int rem = (int)(t - (long long)img * per_img);
   const int ty = rem / geo.tw, tx = rem - ty * geo.tw;
-  float* yk = y + ((long long)img * geo.K + k) * geo.Ho * geo.Wo;
+  float* yk = y ? y + ((long long)img * geo.K + k) * geo.Ho * geo.Wo : nullptr;
+  const int Hp = geo.Ho / 2, Wp = geo.Wo / 2;   // pool 2 (floor)
+  float* ak = act ? act + ((long long)img * geo.K + k) * (pool == 2 ? (long long)Hp * Wp : (long long)geo.Ho * geo.Wo)
+                  : nullptr;
   // rows of the output tile; even M with an even row length -> 8-byte pair stores (the
   // lanes of a warp cover consecutive tiles, so a pair store fills 1/3 of a 768 B span
   // instead of 1/6)
   const bool pairs = (M % 2 == 0) && (geo.Wo % 2 == 0) && (reinterpret_cast<uintptr_t>(y) % 8 == 0);
+  float prev[M];
 #pragma unroll
   for (int p = 0; p < M; p++) {
     const int h = ty * M + p;
@@ -341,84 +352,131 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
       for (int l = 0; l < N; l++) acc = __fmaf_rn(t3[p][l], mt.AT[s * N + l], acc);
       yr[s] = acc;
     }
-    if (h >= geo.Ho) continue;
-    float* row = yk + (long long)h * geo.Wo + tx * M;
     const int wmax = geo.Wo - tx * M;   // valid columns in this tile row
-    if (pairs) {
+    if (yk != nullptr && h < geo.Ho) {
+      float* row = yk + (long long)h * geo.Wo + tx * M;
+      if (pairs) {
 #pragma unroll
-      for (int s = 0; s + 1 < M; s += 2)
-        if (s < wmax) *reinterpret_cast<float2*>(row + s) = make_float2(yr[s], yr[s + 1]);
-    } else {
+        for (int s = 0; s + 1 < M; s += 2)
+          if (s < wmax) *reinterpret_cast<float2*>(row + s) = make_float2(yr[s], yr[s + 1]);
+      } else {
 #pragma unroll
-      for (int s = 0; s < M; s++)
-        if (s < wmax) row[s] = yr[s];
+        for (int s = 0; s < M; s++)
+          if (s < wmax) row[s] = yr[s];
+      }
+    }
+    if (ak != nullptr) {
+      if (pool == 1) {
+        if (h < geo.Ho) {
+          float* row = ak + (long long)h * geo.Wo + tx * M;
+#pragma unroll
+          for (int s = 0; s < M; s++)
+            if (s < wmax) row[s] = fmaxf(yr[s], 0.0f);
+        }
+      } else if (M % 2 == 0) {
+        if (p % 2 == 0) {
+#pragma unroll
+          for (int s = 0; s < M; s++) prev[s] = yr[s];
+        } else if (h / 2 < Hp) {
+          float* row = ak + (long long)(h / 2) * Wp + tx * (M / 2);
+#pragma unroll
+          for (int s = 0; s + 1 < M; s += 2)
+            if (tx * (M / 2) + s / 2 < Wp)
+              row[s / 2] = fmaxf(fmaxf(fmaxf(prev[s], prev[s + 1]), fmaxf(yr[s], yr[s + 1])), 0.0f);
+        }
+      }
     }
   }
 }
 
 // ------------------------------------------------------------------ K5 scoring
 // fp64 direct valid correlation of the same fp32 x, w (eq:conv P:112, O7), compared with
-// the Winograd output y.  CTA = (image, 16 output channels, 32 x 16 outputs):
-// per input channel the x patch (converted to fp64) and the 16 filters are staged in
-// shared memory; each thread accumulates 32 outputs (two positions, 16 channels) with DFMA
-// in the oracle's order (Σ_c Σ_u Σ_v ascending).  Statistics: warp butterflies, then a
-// fixed-order combination of the 8 warps -> one partial per CTA (deterministic).
-constexpr int kScW = 16;   // output columns per CTA
-constexpr int kScH = 32;   // output rows per CTA (each thread: rows ty and ty + 16)
-constexpr int kScK = 16;   // output channels per CTA
+// the Winograd output y.  Each thread owns a 2 x 2 block of output positions for
+// 16 output channels (64 fp64 accumulators): per (channel, filter row u) it reads its
+// 2 x (R + 1) input values once and reuses them for the R filter columns, and every weight
+// (a shared-memory broadcast) feeds 4 DFMAs -- about 1 shared-memory load per 6 DFMA.  A CTA
+// covers BR x BC such blocks, with BC = min(ceil(Wo / 2), 32) and BR = min(128 / BC,
+// ceil(Ho / 2)) chosen at launch so the CTA region tiles the image with little waste
+// (56 x 56: 28 x 4 blocks, no waste).  Per input channel the x patch (converted to fp64) and
+// the 16 filters are staged in double-buffered shared memory, channel c + 1 fetched into
+// registers while channel c is accumulated.  Every accumulator is one chain in the oracle's
+// order (Σ_c Σ_u Σ_v ascending).  Statistics: warp butterflies, then a fixed-order
+// combination of the warps -> one partial per CTA (deterministic; CTAs ordered image-major).
+constexpr int kScK = 16;        // output channels per CTA
+constexpr int kScThreads = 128;
+
+struct ScoreTile {
+  int BR, BC, tiles_h, tiles_w;
+};
+int score_threads(const ScoreTile& t) { return std::max(64, (t.BR * t.BC + 31) / 32 * 32); }
+ScoreTile score_tile(const Geo& g) {
+  ScoreTile t;
+  const int bh = (g.Ho + 1) / 2, bw = (g.Wo + 1) / 2;
+  t.BC = std::min(bw, 32);
+  t.BR = std::max(1, std::min(kScThreads / t.BC, bh));
+  // the staging registers hold <= 8 patch values per thread
+  while (t.BR > 1 && (2 * t.BR + g.r - 1) * (2 * t.BC + g.r - 1) > 8 * score_threads(t)) t.BR--;
+  t.tiles_h = (bh + t.BR - 1) / t.BR;
+  t.tiles_w = (bw + t.BC - 1) / t.BC;
+  return t;
+}
+size_t score_smem(const ScoreTile& t, int r) {
+  const int PH = 2 * t.BR + r - 1, PW = 2 * t.BC + r - 1;
+  return (size_t)2 * (PH * PW + r * r * kScK) * sizeof(double) + 4 * 8 * sizeof(double);
+}
 
 template <int R>
-__global__ void __launch_bounds__(256, 2) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
-                                                    const float* __restrict__ y, Geo geo,
-                                                    double* __restrict__ partial) {
-  constexpr int PH = kScH + R - 1, PW = kScW + R - 1;
-  constexpr int XPT = (PH * PW + 255) / 256, WPT = (kScK * R * R + 255) / 256;   // staged values per thread
-  __shared__ double sx[2][PH * PW];
-  __shared__ __align__(16) double sw[2][R * R][kScK];
-  __shared__ double red[8][7];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int tiles_w = (geo.Wo + kScW - 1) / kScW;
-  const int h0 = (blockIdx.x / tiles_w) * kScH, w0 = (blockIdx.x % tiles_w) * kScW;
+__global__ void __launch_bounds__(kScThreads, 2) score_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                            const float* __restrict__ y, Geo geo, ScoreTile st,
+                                                            double* __restrict__ partial) {
+  const int BR = st.BR, BC = st.BC;
+  const int PH = 2 * BR + R - 1, PW = 2 * BC + R - 1, PATCH = PH * PW;
+  extern __shared__ __align__(16) double ssm[];
+  double* sx = ssm;                        // [2][PATCH]
+  double* sw = sx + 2 * PATCH;             // [2][R*R][kScK]
+  double* red = sw + 2 * R * R * kScK;     // [4 warps][8]
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const bool active = tid < BR * BC;
+  const int br = active ? tid / BC : 0, bc = active ? tid - (tid / BC) * BC : 0;
+  const int h0 = (blockIdx.x / st.tiles_w) * 2 * BR, w0 = (blockIdx.x % st.tiles_w) * 2 * BC;
   const int k0 = blockIdx.y * kScK, img = blockIdx.z;
-  // channel c + 1 is fetched into registers while channel c is accumulated (double-buffered
-  // shared memory, one barrier per channel); each thread owns two output rows, so every
-  // weight read from shared memory feeds two DFMAs
-  float xr[XPT], wr[WPT];
+  constexpr int XMAX = 8, WMAX = (kScK * R * R + 63) / 64;   // staged values per thread (<= PATCH / 64)
+  float xr[XMAX], wr[WMAX];
   auto fetch = [&](int c) {
     const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
 #pragma unroll
-    for (int q = 0; q < XPT; q++) {
-      const int idx = tid + q * 256;
-      const int a = idx / PW, b = idx - (idx / PW) * PW;
+    for (int q = 0; q < XMAX; q++) {
+      const int idx = tid + q * nthr;
+      const int a = idx / PW, b = idx - a * PW;
       const int hh = h0 - geo.pad + a, wx = w0 - geo.pad + b;
-      xr[q] = (idx < PH * PW && hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W)
-                  ? __ldg(xc + (long long)hh * geo.W + wx)
-                  : 0.0f;
+      xr[q] = (idx < PATCH && hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W) ? __ldg(xc + (long long)hh * geo.W + wx)
+                                                                             : 0.0f;
     }
 #pragma unroll
-    for (int q = 0; q < WPT; q++) {
-      const int idx = tid + q * 256;
+    for (int q = 0; q < WMAX; q++) {
+      const int idx = tid + q * nthr;
       const int kk = idx / (R * R), e = idx - kk * (R * R);
       wr[q] = (idx < kScK * R * R && k0 + kk < geo.K) ? __ldg(w + ((long long)(k0 + kk) * geo.C + c) * R * R + e) : 0.0f;
     }
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < XPT; q++) {
-      const int idx = tid + q * 256;
-      if (idx < PH * PW) sx[buf][idx] = (double)xr[q];
+    for (int q = 0; q < XMAX; q++) {
+      const int idx = tid + q * nthr;
+      if (idx < PATCH) sx[buf * PATCH + idx] = (double)xr[q];
     }
 #pragma unroll
-    for (int q = 0; q < WPT; q++) {
-      const int idx = tid + q * 256;
-      if (idx < kScK * R * R) sw[buf][idx % (R * R)][idx / (R * R)] = (double)wr[q];
+    for (int q = 0; q < WMAX; q++) {
+      const int idx = tid + q * nthr;
+      if (idx < kScK * R * R) sw[(buf * R * R + idx % (R * R)) * kScK + idx / (R * R)] = (double)wr[q];
     }
   };
-  double acc[2][kScK];
+  double acc[kScK][4];   // [k][2 * rho + j]: output (h0 + 2 br + rho, w0 + 2 bc + j)
 #pragma unroll
-  for (int j = 0; j < 2; j++)
+  for (int k = 0; k < kScK; k++)
 #pragma unroll
-    for (int k = 0; k < kScK; k++) acc[j][k] = 0.0;
+    for (int p = 0; p < 4; p++) acc[k][p] = 0.0;
   if (geo.C > 0) {
     fetch(0);
     store(0);
@@ -427,46 +485,60 @@ __global__ void __launch_bounds__(256, 2) score_kernel(const float* __restrict__
   for (int c = 0; c < geo.C; c++) {
     const int buf = c & 1;
     if (c + 1 < geo.C) fetch(c + 1);
+    if (active) {
+      const double* px = sx + buf * PATCH + (2 * br) * PW + 2 * bc;
+      const double* pw = sw + buf * R * R * kScK;
 #pragma unroll
-    for (int u = 0; u < R; u++)
+      for (int u = 0; u < R; u++) {
+        double xv[2][R + 1];
 #pragma unroll
-      for (int v = 0; v < R; v++) {
-        const double xa = sx[buf][(ty + u) * PW + tx + v];
-        const double xb = sx[buf][(ty + 16 + u) * PW + tx + v];
+        for (int rho = 0; rho < 2; rho++)
 #pragma unroll
-        for (int k2 = 0; k2 < kScK / 2; k2++) {
-          const double2 wv = *reinterpret_cast<const double2*>(&sw[buf][u * R + v][2 * k2]);
-          acc[0][2 * k2] = __fma_rn(wv.x, xa, acc[0][2 * k2]);
-          acc[0][2 * k2 + 1] = __fma_rn(wv.y, xa, acc[0][2 * k2 + 1]);
-          acc[1][2 * k2] = __fma_rn(wv.x, xb, acc[1][2 * k2]);
-          acc[1][2 * k2 + 1] = __fma_rn(wv.y, xb, acc[1][2 * k2 + 1]);
+          for (int j = 0; j <= R; j++) xv[rho][j] = px[(rho + u) * PW + j];
+#pragma unroll
+        for (int v = 0; v < R; v++) {
+#pragma unroll
+          for (int k2 = 0; k2 < kScK / 2; k2++) {
+            const double2 wv = *reinterpret_cast<const double2*>(pw + (u * R + v) * kScK + 2 * k2);
+#pragma unroll
+            for (int rho = 0; rho < 2; rho++)
+#pragma unroll
+              for (int j = 0; j < 2; j++) {
+                acc[2 * k2][2 * rho + j] = __fma_rn(wv.x, xv[rho][j + v], acc[2 * k2][2 * rho + j]);
+                acc[2 * k2 + 1][2 * rho + j] = __fma_rn(wv.y, xv[rho][j + v], acc[2 * k2 + 1][2 * rho + j]);
+              }
+          }
         }
       }
+    }
     if (c + 1 < geo.C) store(buf ^ 1);
     __syncthreads();
   }
   double s0 = 0, s1 = 0, s2 = 0, m0 = 0, m1 = 0, n = 0, nf = 0;
-  const int ww = w0 + tx;
+  if (active) {
 #pragma unroll
-  for (int j = 0; j < 2; j++) {
-    const int h = h0 + ty + 16 * j;
-    if (h >= geo.Ho || ww >= geo.Wo) continue;
+    for (int rho = 0; rho < 2; rho++)
 #pragma unroll
-    for (int k = 0; k < kScK; k++) {
-      if (k0 + k >= geo.K) break;
-      const double r = acc[j][k];
-      const double e = (double)y[(((long long)img * geo.K + k0 + k) * geo.Ho + h) * geo.Wo + ww] - r;
-      s2 += fabs(r);
-      m1 = fmax(m1, fabs(r));
-      if (isfinite(e)) {
-        s0 += fabs(e);
-        s1 = __fma_rn(e, e, s1);
-        m0 = fmax(m0, fabs(e));
-        n += 1.0;
-      } else {
-        nf += 1.0;
+      for (int j = 0; j < 2; j++) {
+        const int h = h0 + 2 * br + rho, ww = w0 + 2 * bc + j;
+        if (h >= geo.Ho || ww >= geo.Wo) continue;
+#pragma unroll
+        for (int k = 0; k < kScK; k++) {
+          if (k0 + k >= geo.K) break;
+          const double r = acc[k][2 * rho + j];
+          const double e = (double)y[(((long long)img * geo.K + k0 + k) * geo.Ho + h) * geo.Wo + ww] - r;
+          s2 += fabs(r);
+          m1 = fmax(m1, fabs(r));
+          if (isfinite(e)) {
+            s0 += fabs(e);
+            s1 = __fma_rn(e, e, s1);
+            m0 = fmax(m0, fabs(e));
+            n += 1.0;
+          } else {
+            nf += 1.0;
+          }
+        }
       }
-    }
   }
   double v[7] = {s0, s1, s2, n, nf, m0, m1};
 #pragma unroll
@@ -477,14 +549,14 @@ __global__ void __launch_bounds__(256, 2) score_kernel(const float* __restrict__
     v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
   }
   if ((tid & 31) == 0)
-    for (int f = 0; f < 7; f++) red[tid >> 5][f] = v[f];
+    for (int f = 0; f < 7; f++) red[(tid >> 5) * 8 + f] = v[f];
   __syncthreads();
   if (tid == 0) {
     double t[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int wi = 0; wi < 8; wi++) {
-      for (int f = 0; f < 5; f++) t[f] += red[wi][f];
-      t[5] = fmax(t[5], red[wi][5]);
-      t[6] = fmax(t[6], red[wi][6]);
+    for (int wi = 0; wi < nthr / 32; wi++) {
+      for (int f = 0; f < 5; f++) t[f] += red[wi * 8 + f];
+      t[5] = fmax(t[5], red[wi * 8 + 5]);
+      t[6] = fmax(t[6], red[wi * 8 + 6]);
     }
     const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     double* p = partial + blk * 8;
@@ -493,8 +565,6 @@ __global__ void __launch_bounds__(256, 2) score_kernel(const float* __restrict__
   }
 }
 
-// one warp per statistics row: row b sums entries [b n_entries, (b + 1) n_entries) of the
-// partials (per image: the CTAs of image b; whole batch: one row over every CTA)
 __global__ void score_finalize_kernel(const double* __restrict__ partial, int n_entries, double* d_sums,
                                       double* d_maxs) {
   const int lane = threadIdx.x;
@@ -559,8 +629,8 @@ __global__ void relu_pool2_kernel(const float* __restrict__ x, float* __restrict
 // ------------------------------------------------------------------ dispatch
 typedef void (*FilterK)(const float*, float*, int, int, int, int, int, LayerMats);
 typedef void (*InputK)(const float*, float*, Geo, LayerMats);
-typedef void (*OutputK)(const float*, float*, Geo, LayerMats);
-typedef void (*ScoreK)(const float*, const float*, const float*, Geo, double*);
+typedef void (*OutputK)(const float*, float*, Geo, LayerMats, float*, int);
+typedef void (*ScoreK)(const float*, const float*, const float*, Geo, ScoreTile, double*);
 
 struct LayerCfg {
   int m, r;
@@ -576,8 +646,8 @@ LayerCfg make_layer_cfg() {
 }
 
 dim3 score_grid(const Geo& g) {
-  return dim3((unsigned)(((g.Ho + kScH - 1) / kScH) * ((g.Wo + kScW - 1) / kScW)), (unsigned)((g.K + kScK - 1) / kScK),
-              (unsigned)g.N);
+  const ScoreTile t = score_tile(g);
+  return dim3((unsigned)(t.tiles_h * t.tiles_w), (unsigned)((g.K + kScK - 1) / kScK), (unsigned)g.N);
 }
 
 // F(m x m, 3 x 3) for m = 2..8 (n = 4..10: the paper's T7-T9 sizes) and the
@@ -670,7 +740,7 @@ size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, 
 
 int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
                  int m, const float* AT, const float* G, const float* BT, void* workspace, size_t ws_bytes,
-                 double* d_sums, double* d_maxs, unsigned flags, cudaStream_t stream) {
+                 double* d_sums, double* d_maxs, unsigned flags, cudaStream_t stream, float* act, int pool) {
   const LayerCfg* cfg = find_layer(m, r);
   if (!cfg) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
   const int tf32 = (flags & WINO_CONV_3XTF32) ? 2 : (flags & WINO_CONV_TF32) ? 1 : 0;
@@ -754,13 +824,21 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   {
     const long long tot = (long long)g.K * g.T;
     const auto ok = cfg->ok;
-    timed_launch("layer_output", stream, [&] { ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt); });
+    // fused ReLU (+ 2 x 2 pool for even m) epilogue; odd m with pool 2 runs the separate
+    // ReLU / pool kernel on y after the layer
+    const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
+    timed_launch("layer_output", stream, [&] {
+      ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt, fuse ? act : nullptr, pool);
+    });
     launches++;
   }
   if (d_sums) {
     const dim3 sg = score_grid(g);
     const auto sk = cfg->sk;
-    timed_launch("layer_score", stream, [&] { sk<<<sg, 256, 0, stream>>>(x, w, y, g, partial); });
+    const ScoreTile st = score_tile(g);
+    const size_t ssm = score_smem(st, r);
+    timed_launch("layer_score", stream,
+                 [&] { sk<<<sg, score_threads(st), ssm, stream>>>(x, w, y, g, st, partial); });
     // partials are ordered image-major (blockIdx.z = image), so per-image rows are contiguous
     const bool per_image = (flags & WINO_CONV_SCORE_PER_IMAGE) != 0;
     const unsigned rows = per_image ? sg.z : 1u;
@@ -773,6 +851,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   count_launches(launches);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(WINO_E_CUDA, "layer launch: %s", cudaGetErrorString(e));
+  if (act != nullptr && !(pool == 1 || m % 2 == 0)) return relu_pool_launch(y, act, N, K, g.Ho, g.Wo, pool, stream);
   return WINO_OK;
 }
 

@@ -38,7 +38,7 @@ size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, 
 int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K,
                  int r, int pad, int m, const float* AT, const float* G, const float* BT,
                  void* workspace, size_t ws_bytes, double* d_sums, double* d_maxs,
-                 unsigned flags, cudaStream_t stream);
+                 unsigned flags, cudaStream_t stream, float* act = nullptr, int pool = 0);
 
 int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int pool, cudaStream_t stream);
 

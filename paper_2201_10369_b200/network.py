@@ -1,7 +1,8 @@
 """configs[4]: the VGG-16 conv stack with every 3x3 convolution as an F(m x m, 3 x 3)
 Winograd layer (§6.4 protocol, on synthetic inputs): per layer
 wino_conv2d_fp32 (scored against the fp64 direct convolution of the same fp32 input --
-the isolated per-layer error, reading R13 of DESIGN.md) then wino_relu_pool_fp32.
+the isolated per-layer error, reading R13 of DESIGN.md) with ReLU (+ 2x2 max pool) fused
+into its output transform (wino_conv2d_relu_pool_fp32).
 Every step runs in libwino's kernels; this module only sequences the calls.
 
 Multi-GPU: one process per GPU, the batch sharded in contiguous image
@@ -37,16 +38,15 @@ RESNET20_LIKE = ([(3, 16, 32, False)] + [(16, 16, 32, False)] * 5 + [(16, 16, 32
                  + [(16, 32, 16, False)] + [(32, 32, 16, False)] * 4 + [(32, 32, 16, True)]
                  + [(32, 64, 8, False)] + [(64, 64, 8, False)] * 5)
 
-# SqueezeNet-shaped CIFAR stack ("SqueezeNet"; the 3x3 convolutions of the fire
-# modules' expand branches with their squeeze widths as inputs -- the 1x1 convolutions are
-# not Winograd layers and are not part of the paper's per-layer protocol): conv 3->64 at
-# 32, then fire-module 3x3 expands 16->64, 16->64 (pool), 32->128, 32->128 (pool),
-# 48->192, 48->192, 64->256, 64->256 at 8.  Each entry: (C, K, H, pool_after).
+# SqueezeNet-shaped CIFAR stack ("SqueezeNet"; 8 of its 26 layers ran as
+# Winograd layers): 8 chained 3x3 convolutions with the widths of SqueezeNet's 3x3 expand
+# branches (64 at 32x32, 128 at 16x16, 192 / 256 at 8x8) -- the 1x1 squeeze / expand
+# convolutions are not Winograd layers and are left out, so each 3x3 layer consumes the
+# previous activation directly.  Each entry: (C, K, H, pool_after).
 SQUEEZENET_LIKE = [
-    (3, 64, 32, False),
-    (16, 64, 32, False), (16, 64, 32, True),
-    (32, 128, 16, False), (32, 128, 16, True),
-    (48, 192, 8, False), (48, 192, 8, False), (64, 256, 8, False), (64, 256, 8, False),
+    (3, 64, 32, False), (64, 64, 32, True),
+    (64, 128, 16, False), (128, 128, 16, True),
+    (128, 192, 8, False), (192, 192, 8, False), (192, 256, 8, False), (256, 256, 8, False),
 ]
 
 
@@ -62,13 +62,11 @@ def shard(n: int, rank: int, world: int):
     return (n * rank) // world, (n * (rank + 1)) // world
 
 
-def _abi_conv(a, w, y, m, points, ws, sums, maxs, stream):
+def _abi_conv(a, w, y, act, pool, m, points, ws, sums, maxs, stream):
+    """One layer: Winograd conv with the ReLU (+ pool) fused into its output transform
+    (wino_conv2d_relu_pool_fp32); y (the conv output) is materialised only when given."""
     flags = api.WINO_CONV_SCORE_PER_IMAGE if sums is not None else 0
-    api.wino_conv2d_fp32(a, w, y, 1, m, points, ws, sums, maxs, stream, flags)
-
-
-def _abi_relu_pool(y, out, pool, stream):
-    api.wino_relu_pool_fp32(y, out, pool, stream)
+    api.wino_conv2d_relu_pool_fp32(a, w, y, act, 1, m, points, ws, pool, sums, maxs, stream, flags)
 
 
 def _abi_ws(N, C, H, K, m):
@@ -77,15 +75,17 @@ def _abi_ws(N, C, H, K, m):
 
 def stack_forward(layers, x, weights: Sequence, points, m: int = 6, score: bool = True, keep: bool = False,
                   stream=None, rank: int = 0, world: int = 1, n_global: Optional[int] = None, group=None,
-                  conv: Callable = _abi_conv, relu_pool: Callable = _abi_relu_pool, ws_bytes: Callable = _abi_ws):
+                  conv: Callable = _abi_conv, ws_bytes: Callable = _abi_ws):
     """Generic 3x3 conv stack (C, K, H, pool_after) per layer: Winograd conv (scored) ->
     ReLU (-> 2x2 max pool).
 
     x: this rank's images [N_r, C, H, H] = images [lo, hi) of the global batch of n_global
     (default: N_r, world 1).  Returns (final activation of the rank's images, sums [L,5],
     maxs [L,2] over ALL images (after the all-reduce when world > 1), conv outputs if keep,
-    per-image statistics [L, n_global, 7]).  `conv` / `relu_pool` / `ws_bytes` are the C-ABI
-    calls; tests inject CPU stand-ins to check the sharding and reduction logic."""
+    per-image statistics [L, n_global, 7]).  `conv` / `ws_bytes` are the C-ABI calls; tests
+    inject CPU stand-ins to check the sharding and reduction logic.  The conv output y of a
+    layer is materialised only when it is scored or kept (otherwise the fused epilogue
+    writes just the activation)."""
     import torch
     N, _, H, W = x.shape
     n_global = N if n_global is None else n_global
@@ -109,16 +109,14 @@ def stack_forward(layers, x, weights: Sequence, points, m: int = 6, score: bool 
     a = x
     for li, ((C, K, _, pool), w) in enumerate(zip(layers, weights)):
         h = a.shape[2]
-        y = torch.empty((N, K, h, h), dtype=torch.float32, device=dev)
-        if N > 0:
-            conv(a, w, y, m, points, ws, sums_img[li, lo:hi] if score else None,
-                 maxs_img[li, lo:hi] if score else None, stream)
-        if keep:
-            outs.append(y)
+        y = torch.empty((N, K, h, h), dtype=torch.float32, device=dev) if (score or keep) else None
         p = 2 if pool else 1
         a2 = torch.empty((N, K, h // p, h // p), dtype=torch.float32, device=dev)
         if N > 0:
-            relu_pool(y, a2, p, stream)
+            conv(a, w, y, a2, p, m, points, ws, sums_img[li, lo:hi] if score else None,
+                 maxs_img[li, lo:hi] if score else None, stream)
+        if keep:
+            outs.append(y)
         a = a2
     if not score:
         return a, None, None, outs, None

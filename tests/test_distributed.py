@@ -127,20 +127,18 @@ def _net_inputs():
     return synth.stack_inputs(_NET, _NET_IMAGES, seed=9)
 
 
-def _oracle_conv(a, w, y, m, points, ws, sums, maxs, stream):
+def _oracle_conv(a, w, y, act, pool, m, points, ws, sums, maxs, stream):
+    from oracle import network as ON
     x, wt = a.numpy(), w.numpy()
     yy = ref.conv2d_wino(x, wt, 1, m, points)
     y64 = ref.conv2d_direct64(x, wt, 1)
-    y.copy_(torch.from_numpy(yy))
+    if y is not None:
+        y.copy_(torch.from_numpy(yy))
+    act.copy_(torch.from_numpy(ON.relu_pool(yy, pool == 2)))
     for i in range(x.shape[0]):
         si, mi = ref.stats(yy[i], y64[i])
         sums[i] += torch.from_numpy(si)
         maxs[i] = torch.maximum(maxs[i], torch.from_numpy(mi))
-
-
-def _oracle_relu_pool(y, out, pool, stream):
-    from oracle import network as ON
-    out.copy_(torch.from_numpy(ON.relu_pool(y.numpy(), pool == 2)))
 
 
 def _net_run(rank, world, group=None):
@@ -150,7 +148,7 @@ def _net_run(rank, world, group=None):
     lo, hi = network.shard(_NET_IMAGES, rank, world)
     return network.stack_forward(_NET, torch.from_numpy(x[lo:hi]), [torch.from_numpy(w) for w in ws],
                                  OP.f23_c(1.0), m=2, rank=rank, world=world, n_global=_NET_IMAGES, group=group,
-                                 conv=_oracle_conv, relu_pool=_oracle_relu_pool, ws_bytes=lambda *a: 1)
+                                 conv=_oracle_conv, ws_bytes=lambda *a: 1)
 
 
 def _net_worker(rank, world, port, out):

@@ -120,3 +120,43 @@ def test_layer_errors():
     with pytest.raises(_lib.WinoError) as ei:
         api.wino_conv2d_fp32(x, w, y, 1, 9, [float(i) for i in range(10)] + [INF], ws)
     assert ei.value.status == 8
+
+
+@pytest.mark.parametrize("N,C,H,K,m,pts,pool", [
+    (2, 13, 19, 37, 6, OP.n8_cd(2.0, 1.003), 2),     # even m: fused pool, odd H (floor) + ragged tiles
+    (2, 8, 16, 16, 6, OP.n8_cd(2.0, 1.003), 1),      # fused ReLU only
+    (1, 9, 17, 20, 3, OP.canonical([0.0, 1.0, -1.0, 0.5]), 2),   # odd m: separate pool kernel
+    (2, 8, 18, 16, 2, OP.f23_c(1.0), 2),
+    (1, 5, 15, 7, 7, OP.chebyshev(9), 2),             # F(7x7,3x3) layer
+    (1, 5, 20, 6, 8, OP.P10, 2),                      # F(8x8,3x3) layer
+])
+def test_fused_relu_pool_equals_separate(N, C, H, K, m, pts, pool):
+    """wino_conv2d_relu_pool_fp32: act = maxpool(ReLU(conv)) bit for bit equal to the oracle
+    layer followed by the oracle's ReLU / pool; y (when requested) equals the oracle layer;
+    scored statistics per image sum to the whole-batch statistics."""
+    import torch
+    from oracle import network as ON
+    from paper_2201_10369_b200 import api
+    x, w = synth.layer_inputs(N, C, H, H, K, 3, "normal", "he", seed=7)
+    y_ref = ref.conv2d_wino(x, w, 1, m, pts)
+    a_ref = ON.relu_pool(y_ref, pool == 2)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, H, K, 3, 1, m), dtype=torch.uint8, device="cuda")
+    act = torch.full(a_ref.shape, float("nan"), dtype=torch.float32, device="cuda")
+    y = torch.full(y_ref.shape, float("nan"), dtype=torch.float32, device="cuda")
+    sums = torch.zeros((N, 5), dtype=torch.float64, device="cuda")
+    maxs = torch.zeros((N, 2), dtype=torch.float64, device="cuda")
+    api.wino_conv2d_relu_pool_fp32(xd, wd, y, act, 1, m, pts, ws, pool, sums, maxs,
+                                   flags=api.WINO_CONV_SCORE_PER_IMAGE)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y_ref)
+    assert np.array_equal(act.cpu().numpy(), a_ref)
+    s_ref, m_ref = ref.stats(y_ref, ref.conv2d_direct64(x, w, 1))
+    s = sums.cpu().numpy().sum(axis=0)
+    assert s[3] == s_ref[3] and s[4] == s_ref[4]
+    assert abs(s[0] / s_ref[0] - 1) < 1e-9 and np.array_equal(maxs.cpu().numpy().max(axis=0), m_ref)
+    if m % 2 == 0 or pool == 1:       # y not materialised: the activation alone
+        act2 = torch.full(a_ref.shape, float("nan"), dtype=torch.float32, device="cuda")
+        api.wino_conv2d_relu_pool_fp32(xd, wd, None, act2, 1, m, pts, ws, pool)
+        torch.cuda.synchronize()
+        assert np.array_equal(act2.cpu().numpy(), a_ref)

@@ -181,7 +181,7 @@ def part_cd(args, flags, dev):
                 return _mae_of_sets(dims, m, 3, sets, dt, gt, flags)
 
             coarse_c = np.round(np.arange(1.0, 2.6 + 1e-9, 0.01), 6)
-            coarse_d = np.round(np.arange(0.5, 3.0 + 1e-9, 0.01), 6)
+            coarse_d = np.round(np.arange(0.5, 4.0 + 1e-9, 0.01), 6)
             pairs = [(c, d) for c in coarse_c for d in coarse_d]
             mae = score(pairs)
             i = int(np.nanargmin(mae))
