@@ -8,7 +8,8 @@
 //   K5 score_kernel  : y64 = fp64 direct correlation (eq:conv P:112), e = y - y64,
 //                      per-warp statistics (warp shuffles), fixed grid
 //   K8 finalize      : fixed-order reduction into d_sums/d_maxs
-// Cp = C rounded up to 16, Kp = K and Tp = T rounded up to 128; padding is zero-filled
+// Cp = C rounded up to 16, Kp = K rounded up to 128 (64 when K <= 64), Tp = T rounded up to
+// 128; padding is zero-filled
 // by K1/K2, so K3 needs no bounds checks (an fma(0, 0, acc) leaves acc unchanged up to
 // the sign of a zero).  Parity semantics: every dot product is an
 // fmaf chain from +0 in ascending index order, 2D transforms left product first.
@@ -62,7 +63,8 @@ Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, int tf32 
   // FFMA GEMM: BK = 16, BN = 128; tcgen05 variant: BK = 32, N = 256
   const int ca = tf32 ? 32 : 16, ta = tf32 ? 256 : 128;
   g.Cp = (C + ca - 1) / ca * ca;
-  g.Kp = (K + 127) / 128 * 128;
+  // FFMA GEMM: 64-row tiles when K <= 64 (VGG's 64-channel layers), else 128; tcgen05: 128
+  g.Kp = (!tf32 && K <= 64) ? 64 : (K + 127) / 128 * 128;
   g.Tp = (g.T + ta - 1) / ta * ta;
   g.tf32 = tf32;
   return g;
@@ -201,10 +203,11 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
 }
 
 // ------------------------------------------------------------------ K3
-// Batched SGEMM  M_p[k][t] = Σ_c U_p[c][k] V_p[c][t], 128 x 128 CTA tile, BK = 8,
-// 256 threads x (8 x 8) register tile, accumulators as FFMA2 pairs along t.
-// cp.async double-buffered shared memory; every accumulator is one ascending-c fmaf chain.
-constexpr int BM = 128, BN = 128, BK = 16;
+// Batched SGEMM  M_p[k][t] = Σ_c U_p[c][k] V_p[c][t], BMT x 128 CTA tile (BMT = 128, or 64
+// when K <= 64 so the GEMM neither computes nor writes padded k rows), BK = 16,
+// 2 * BMT threads x (8 x 8) register tile, accumulators as FFMA2 pairs along t.
+// cp.async 3-stage shared-memory ring; every accumulator is one ascending-c fmaf chain.
+constexpr int BN = 128, BK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -222,22 +225,26 @@ __device__ __forceinline__ u64 ffma2_bcast(u64 a, float c, u64 acc) {
 }
 
 constexpr int kStages = 3;
-constexpr size_t kGemmSmem = (size_t)kStages * BK * (BM + BN) * sizeof(float);
+template <int BMT>
+constexpr size_t gemm_smem() { return (size_t)kStages * BK * (BMT + BN) * sizeof(float); }
 
-__global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ U, const float* __restrict__ V,
-                                                      float* __restrict__ Mo, int Cp, int Kp, long long Tp) {
+template <int BMT>
+__global__ void __launch_bounds__(2 * BMT, 256 / BMT) gemm_kernel(const float* __restrict__ U,
+                                                                 const float* __restrict__ V, float* __restrict__ Mo,
+                                                                 int Cp, int Kp, long long Tp) {
+  constexpr int NT = 2 * BMT;                 // threads
+  constexpr int AV = BK * BMT / 4 / NT;       // float4 per thread per stage (A)
+  constexpr int BV = BK * BN / 4 / NT;        // (B)
   extern __shared__ __align__(16) float gsm[];
-  float (*As)[BK][BM] = reinterpret_cast<float (*)[BK][BM]>(gsm);
-  float (*Bs)[BK][BN] = reinterpret_cast<float (*)[BK][BN]>(gsm + kStages * BK * BM);
+  float (*As)[BK][BMT] = reinterpret_cast<float (*)[BK][BMT]>(gsm);
+  float (*Bs)[BK][BN] = reinterpret_cast<float (*)[BK][BN]>(gsm + kStages * BK * BMT);
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  const int tx = tid & 15, ty = tid >> 4;     // ty < BMT / 8
   const long long t0 = (long long)blockIdx.x * BN;
-  const int k0 = blockIdx.y * BM;
+  const int k0 = blockIdx.y * BMT;
   const int p = blockIdx.z;
   const float* Ap = U + (long long)p * Cp * Kp + k0;
   const float* Bp = V + (long long)p * Cp * Tp + t0;
-  // loader mapping: 256 threads x 2 float4 = 16 rows x 128 columns per operand
-  const int lr = tid >> 5, lc = (tid & 31) * 4;
 
   u64 acc[8][4];
 #pragma unroll
@@ -248,10 +255,16 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
   const int nk = Cp / BK;
   auto load = [&](int stage, int kt) {
 #pragma unroll
-    for (int h = 0; h < BK / 8; h++) {
-      const long long c = (long long)kt * BK + lr + 8 * h;
-      cp_async16(&As[stage][lr + 8 * h][lc], Ap + c * Kp + lc);
-      cp_async16(&Bs[stage][lr + 8 * h][lc], Bp + c * Tp + lc);
+    for (int h = 0; h < AV; h++) {
+      const int f = tid + h * NT;               // float4 index in the BK x BMT tile
+      const int row = f / (BMT / 4), col = (f % (BMT / 4)) * 4;
+      cp_async16(&As[stage][row][col], Ap + ((long long)kt * BK + row) * Kp + col);
+    }
+#pragma unroll
+    for (int h = 0; h < BV; h++) {
+      const int f = tid + h * NT;
+      const int row = f / (BN / 4), col = (f % (BN / 4)) * 4;
+      cp_async16(&Bs[stage][row][col], Bp + ((long long)kt * BK + row) * Tp + col);
     }
   };
   load(0, 0);
@@ -267,7 +280,7 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
 #pragma unroll
     for (int kk = 0; kk < BK; kk++) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][64 + ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][BMT / 2 + ty * 4]);
       const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][tx * 4]);
       const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][64 + tx * 4]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -281,7 +294,7 @@ __global__ void __launch_bounds__(256, 2) gemm_kernel(const float* __restrict__ 
   float* Mp = Mo + (long long)p * Kp * Tp;
 #pragma unroll
   for (int i = 0; i < 8; i++) {
-    const int k = k0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    const int k = k0 + (i < 4 ? ty * 4 + i : BMT / 2 + ty * 4 + (i - 4));
     float* row = Mp + (long long)k * Tp + t0;
     *reinterpret_cast<ulonglong2*>(row + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
     *reinterpret_cast<ulonglong2*>(row + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
@@ -442,23 +455,31 @@ __global__ void __launch_bounds__(kScThreads, 2) score_kernel(const float* __res
   const int h0 = (blockIdx.x / st.tiles_w) * 2 * BR, w0 = (blockIdx.x % st.tiles_w) * 2 * BC;
   const int k0 = blockIdx.y * kScK, img = blockIdx.z;
   constexpr int XMAX = 8, WMAX = (kScK * R * R + 63) / 64;   // staged values per thread (<= PATCH / 64)
+  // channel-independent staging geometry, computed once (no integer divisions per channel):
+  // x: offset inside the channel plane (-1 = zero padding / beyond the patch); w: offset
+  // relative to channel 0 (-1 = beyond the CTA's channels) and the shared-memory slot
+  int xoff[XMAX], woff[WMAX], wslot[WMAX];
+#pragma unroll
+  for (int q = 0; q < XMAX; q++) {
+    const int idx = tid + q * nthr;
+    const int a = idx / PW, b = idx - a * PW;
+    const int hh = h0 - geo.pad + a, wx = w0 - geo.pad + b;
+    xoff[q] = (idx < PATCH && hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W) ? hh * geo.W + wx : -1;
+  }
+#pragma unroll
+  for (int q = 0; q < WMAX; q++) {
+    const int idx = tid + q * nthr;
+    const int kk = idx / (R * R), e = idx - kk * (R * R);
+    woff[q] = (idx < kScK * R * R && k0 + kk < geo.K) ? (k0 + kk) * geo.C * R * R + e : -1;
+    wslot[q] = idx < kScK * R * R ? e * kScK + kk : -1;
+  }
   float xr[XMAX], wr[WMAX];
   auto fetch = [&](int c) {
     const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W;
 #pragma unroll
-    for (int q = 0; q < XMAX; q++) {
-      const int idx = tid + q * nthr;
-      const int a = idx / PW, b = idx - a * PW;
-      const int hh = h0 - geo.pad + a, wx = w0 - geo.pad + b;
-      xr[q] = (idx < PATCH && hh >= 0 && hh < geo.H && wx >= 0 && wx < geo.W) ? __ldg(xc + (long long)hh * geo.W + wx)
-                                                                             : 0.0f;
-    }
+    for (int q = 0; q < XMAX; q++) xr[q] = xoff[q] >= 0 ? __ldg(xc + xoff[q]) : 0.0f;
 #pragma unroll
-    for (int q = 0; q < WMAX; q++) {
-      const int idx = tid + q * nthr;
-      const int kk = idx / (R * R), e = idx - kk * (R * R);
-      wr[q] = (idx < kScK * R * R && k0 + kk < geo.K) ? __ldg(w + ((long long)(k0 + kk) * geo.C + c) * R * R + e) : 0.0f;
-    }
+    for (int q = 0; q < WMAX; q++) wr[q] = woff[q] >= 0 ? __ldg(w + woff[q] + (long long)c * R * R) : 0.0f;
   };
   auto store = [&](int buf) {
 #pragma unroll
@@ -467,10 +488,8 @@ __global__ void __launch_bounds__(kScThreads, 2) score_kernel(const float* __res
       if (idx < PATCH) sx[buf * PATCH + idx] = (double)xr[q];
     }
 #pragma unroll
-    for (int q = 0; q < WMAX; q++) {
-      const int idx = tid + q * nthr;
-      if (idx < kScK * R * R) sw[(buf * R * R + idx % (R * R)) * kScK + idx / (R * R)] = (double)wr[q];
-    }
+    for (int q = 0; q < WMAX; q++)
+      if (wslot[q] >= 0) sw[buf * R * R * kScK + wslot[q]] = (double)wr[q];
   };
   double acc[kScK][4];   // [k][2 * rho + j]: output (h0 + 2 br + rho, w0 + 2 bc + j)
 #pragma unroll
@@ -814,10 +833,21 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
         kern<<<grid, tc::kThreads, smem, stream>>>(tmU, tmV, tmUl, tmVl, tmM, g.Cp, g.Kp, g.Tp, n * n);
       });
     } else {
-      dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / BM), (unsigned)(n * n));
-      cudaFuncSetAttribute((const void*)gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      timed_launch("layer_gemm", stream,
-                   [&] { gemm_kernel<<<grid, 256, kGemmSmem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
+      if (g.Kp == 64) {
+        dim3 grid((unsigned)(g.Tp / BN), 1u, (unsigned)(n * n));
+        cudaFuncSetAttribute((const void*)gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<64>());
+        timed_launch("layer_gemm", stream, [&] {
+          gemm_kernel<64><<<grid, 128, gemm_smem<64>(), stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+        });
+      } else {
+        dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / 128), (unsigned)(n * n));
+        cudaFuncSetAttribute((const void*)gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<128>());
+        timed_launch("layer_gemm", stream, [&] {
+          gemm_kernel<128><<<grid, 256, gemm_smem<128>(), stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+        });
+      }
     }
     launches++;
   }

@@ -27,6 +27,25 @@ def main():
         for _ in range(2):
             run_step(rs)
         torch.cuda.synchronize()
+    if what == "cfg4":    # configs[3] grid sweeps, a 24 x 24 sub-grid of (c1, c2) at 100k tiles
+        from paper_2201_10369_b200.sweep import SweepSpec
+        g = synth.c_grid(24)
+        params = np.array([(a, b) for a in g for b in g if a != b], dtype=np.float64)
+        rs = []
+        for tpl in ("n8_c1c2_r5", "n10_c1c2_r5"):
+            sp = SweepSpec("cfg4", 2, tpl, params, "uniform", 100_000, seed=2)
+            d, gg = synth.random_tiles(sp.n_tiles, 2, sp.n, sp.r, sp.dist, sp.seed)
+            rs.append(make_rank_sweep(sp, 0, 1, dev, d, gg))
+        for _ in range(2):
+            run_step(rs)
+        torch.cuda.synchronize()
+    if what == "score":   # the configs[2] layer, scored (the fp64 scorer K5)
+        N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
+        x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
+        xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
+        pts = PP.family_n8_cd(2.0, 1.003)
+        y, s, mx = api.conv2d(xd, wd, pad, m, pts, score=True)
+        torch.cuda.synchronize()
     if what in ("all", "layer"):
         N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
         x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
