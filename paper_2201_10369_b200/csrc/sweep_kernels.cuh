@@ -183,28 +183,29 @@ struct Stat {
 // relative of the fp64 definition (tolerance of the north star: 1 %).  A non-finite sum
 // sends the candidate's work item to the exact fp64 careful path.
 struct Stat32 {
-  u64 s0 = 0ull, s1 = 0ull, m0 = 0ull;
+  // Σ|e| per half as scalars (FADD with an |.| operand modifier: no sign-mask LOP3), Σe² as
+  // an FFMA2 pair, max|e| over both halves with one 3-input FMNMX -- the same sums as a
+  // pair-wise accumulation, in fewer issue slots
+  float s0a = 0.0f, s0b = 0.0f, m0 = 0.0f;
+  u64 s1 = 0ull;
   __device__ __forceinline__ void add(u64 y, u64 hi, u64 lo) {
     u64 e, t;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(hi));
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e) : "l"(t), "l"(lo));
-    const u64 ae = e & 0x7fffffff7fffffffull;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s0) : "l"(s0), "l"(ae));
+    float e0, e1;
+    split2(e, e0, e1);
+    s0a = __fadd_rn(s0a, fabsf(e0));
+    s0b = __fadd_rn(s0b, fabsf(e1));
     asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s1) : "l"(e), "l"(s1));
-    float a0, a1, m0a, m0b;
-    split2(ae, a0, a1);
-    split2(m0, m0a, m0b);
-    m0 = pack2(fmaxf(m0a, a0), fmaxf(m0b, a1));
+    m0 = fmaxf(m0, fmaxf(fabsf(e0), fabsf(e1)));
   }
   // the two halves combined (fixed order)
   __device__ __forceinline__ void fold(float& v0, float& v1, float& vm) const {
     float a, b;
-    split2(s0, a, b);
-    v0 = a + b;
+    v0 = s0a + s0b;
     split2(s1, a, b);
     v1 = a + b;
-    split2(m0, a, b);
-    vm = fmaxf(a, b);
+    vm = m0;
   }
 };
 

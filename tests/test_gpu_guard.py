@@ -18,14 +18,15 @@ def _guarded(torch, shape, dtype, fill, guard=4099):
     """A contiguous view of `shape` inside a flat buffer with `guard` sentinel elements on
     both sides.  Returns (view, check) -- check() asserts the guards are intact."""
     n = int(np.prod(shape)) if len(shape) else 1
-    flat = torch.full((n + 2 * guard,), SENT, dtype=dtype, device="cuda")
+    sent = 0xA5 if dtype == torch.uint8 else SENT
+    flat = torch.full((n + 2 * guard,), sent, dtype=dtype, device="cuda")
     view = flat[guard:guard + n].view(*shape)
     view.fill_(fill)
 
     def check():
         torch.cuda.synchronize()
         g = torch.cat([flat[:guard], flat[guard + n:]]).cpu().numpy()
-        assert np.all(g == np.asarray(SENT, dtype=g.dtype)), "write outside the buffer"
+        assert np.all(g == np.asarray(sent, dtype=g.dtype)), "write outside the buffer"
     return view, check
 
 
