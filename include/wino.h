@@ -164,7 +164,8 @@ int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, in
  * sweep; the multi-GPU driver shards candidates over ranks and all-reduces the stats).
  *   dims 1|2; point_sets: HOST double[n_cand][n] (each row obeys (1)).
  *   d_tiles: DEVICE float[n_tiles][n^dims], g_tiles: DEVICE float[n_tiles][r^dims]
- *   (row-major n x n / r x r tiles; the SAME tiles score every candidate, O9).
+ *   (row-major n x n / r x r tiles; the SAME tiles score every candidate, O9), both
+ *   16-byte aligned (vector loads; else WINO_E_INVALID_ARG).
  *   d_sums: DEVICE double[n_cand][WINO_SUMS], d_maxs: DEVICE double[n_cand][WINO_MAXS]
  *   (ACCUMULATED for accepted candidates).  cand_status: HOST int[n_cand] out, per-candidate
  *   wino_status of (1); a rejected candidate does not fail the call and its statistics rows

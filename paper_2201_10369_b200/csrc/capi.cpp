@@ -229,6 +229,10 @@ static int sweep_common(int dims, int m, int r, const double* point_sets, int n_
   if (m < 1 || r < 1 || n_cand < 0 || n_tiles < 0) return set_error(WINO_E_INVALID_ARG, "bad sizes");
   if (n_cand > 0 && (!point_sets || !cand_status)) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
   if (n_cand > 0 && n_tiles > 0 && (!d_tiles || !g_tiles)) return set_error(WINO_E_INVALID_ARG, "NULL tiles");
+  if ((reinterpret_cast<uintptr_t>(d_tiles) | reinterpret_cast<uintptr_t>(g_tiles)) & 15u)
+    return set_error(WINO_E_INVALID_ARG, "d_tiles / g_tiles must be 16-byte aligned (vector loads)");
+  if ((reinterpret_cast<uintptr_t>(d_sums) | reinterpret_cast<uintptr_t>(d_maxs)) & 7u)
+    return set_error(WINO_E_INVALID_ARG, "statistics buffers must be 8-byte aligned");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
   if (flags & ~(WINO_SWEEP_NOFMA | WINO_SWEEP_HUFFMAN | WINO_SWEEP_MIXED))

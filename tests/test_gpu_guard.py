@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 SENT = -12345.678
 
 
-def _guarded(torch, shape, dtype, fill, guard=4099):
+def _guarded(torch, shape, dtype, fill, guard=4096):
     """A contiguous view of `shape` inside a flat buffer with `guard` sentinel elements on
     both sides.  Returns (view, check) -- check() asserts the guards are intact."""
     n = int(np.prod(shape)) if len(shape) else 1
@@ -105,3 +105,22 @@ def test_sweep_statistics_deterministic(dims):
             first = got
         else:
             assert np.array_equal(got, first, equal_nan=True)
+
+
+def test_unaligned_tiles_rejected():
+    """The sweep reads tiles with 16-byte vector loads: a misaligned pointer is refused
+    (WINO_E_INVALID_ARG) instead of faulting on the device."""
+    import torch
+    from paper_2201_10369_b200 import _lib, api
+    d, g = synth.random_tiles(300, 2, 6, 3, "uniform", seed=54)
+    flat = torch.zeros(d.size + 1, dtype=torch.float32, device="cuda")
+    dd = flat[1:].view(d.shape)
+    dd.copy_(torch.from_numpy(d))
+    gg = torch.from_numpy(g).cuda()
+    sums = torch.zeros((1, 5), dtype=torch.float64, device="cuda")
+    maxs = torch.zeros((1, 2), dtype=torch.float64, device="cuda")
+    ws = torch.empty(api.wino_error_sweep_workspace_bytes(2, 4, 3, 1, 300), dtype=torch.uint8, device="cuda")
+    with pytest.raises(_lib.WinoError) as ei:
+        api.wino_error_sweep(2, 4, 3, np.array([OP.f43_c(1.6)]), dd, gg, sums, maxs, ws)
+    assert ei.value.status == 1
+    torch.cuda.synchronize()
