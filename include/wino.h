@@ -170,7 +170,8 @@ int wino_relu_pool_fp32(const float* x, float* y, int N, int C, int H, int W, in
  *   (ACCUMULATED for accepted candidates).  cand_status: HOST int[n_cand] out, per-candidate
  *   wino_status of (1); a rejected candidate does not fail the call and its statistics rows
  *   are OVERWRITTEN with NaN (so a caller can never read a silent 0/0 mean).
- *   workspace: DEVICE, >= wino_error_sweep_workspace_bytes(...).  flags: WINO_SWEEP_*.
+ *   workspace: DEVICE, >= wino_error_sweep_workspace_bytes(...), 256-byte aligned.
+ *   flags: WINO_SWEEP_*.
  * Every output of every tile is scored against the fp64 direct correlation of the tile.
  * A candidate whose outputs are not all finite is scored exactly per output (n_nonfinite
  * counts the non-finite e over the real tiles).  Asynchronous on `stream` (host matrix

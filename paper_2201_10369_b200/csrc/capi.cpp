@@ -167,6 +167,10 @@ static int conv_common(const float* x, const float* w, float* y, float* act, int
   if (!y && (d_sums || (act && pool == 2 && m % 2 != 0)))
     return set_error(WINO_E_INVALID_ARG, "y is required for scoring and for pool 2 with odd m");
   if (H + 2 * pad < r || W + 2 * pad < r) return set_error(WINO_E_BAD_SHAPE, "empty output");
+  if (reinterpret_cast<uintptr_t>(workspace) & 255u)
+    return set_error(WINO_E_WORKSPACE, "workspace must be 256-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(d_sums) | reinterpret_cast<uintptr_t>(d_maxs)) & 7u)
+    return set_error(WINO_E_INVALID_ARG, "statistics buffers must be 8-byte aligned");
   if (act && pool == 2 && (H + 2 * pad - r + 1 < 2 || W + 2 * pad - r + 1 < 2))
     return set_error(WINO_E_BAD_SHAPE, "pool 2 needs an output of at least 2 x 2");
   const int n = m + r - 1;
@@ -233,6 +237,8 @@ static int sweep_common(int dims, int m, int r, const double* point_sets, int n_
     return set_error(WINO_E_INVALID_ARG, "d_tiles / g_tiles must be 16-byte aligned (vector loads)");
   if ((reinterpret_cast<uintptr_t>(d_sums) | reinterpret_cast<uintptr_t>(d_maxs)) & 7u)
     return set_error(WINO_E_INVALID_ARG, "statistics buffers must be 8-byte aligned");
+  if (reinterpret_cast<uintptr_t>(workspace) & 255u)
+    return set_error(WINO_E_WORKSPACE, "workspace must be 256-byte aligned");
   if ((d_sums == nullptr) != (d_maxs == nullptr))
     return set_error(WINO_E_INVALID_ARG, "d_sums and d_maxs must both be NULL or both non-NULL");
   if (flags & ~(WINO_SWEEP_NOFMA | WINO_SWEEP_HUFFMAN | WINO_SWEEP_MIXED))
