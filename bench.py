@@ -460,8 +460,10 @@ def main():
         "mul_per_tile_eval": mul_te, "kernel_ms_total": k2_ms, "launches": k2_n,
         "avg_launch_ms": k2_ms / k2_n if k2_n else None,
         "share_of_step": k2_ms / sum(prof_ms) if prof_ms else None,
-        "timing": "per-launch CUDA events on the launch stream, in a second pass of the same K steps "
-                  "(the headline timed region runs without the hook)",
+        "timing": "CUDA events on the launch stream around each sweep call's PDL chain of candidate-chunk "
+                  "launches of this kernel (events between chained launches would serialise them; 'launches' "
+                  "counts the chained launches), in a second pass of the same K steps (the headline timed "
+                  "region runs without the hook)",
         "profiled_pass_ms_per_step": statistics.mean(prof_ms) if prof_ms else None,
         "other_kernels_ms": {"sweep1d": k1_ms, "sweep_refs2d": kref_ms, "sweep_finalize": kfin_ms},
     }

@@ -201,8 +201,11 @@ int wino_last_launch_count(void);
  * bracketed by two cudaEvents recorded on its own stream and filed under its kernel
  * family: "sweep1d", "sweep2d", "sweep_huffman", "sweep_mixed", "sweep_refs1d", "sweep_refs2d", "sweep_finalize",
  * "layer_filter", "layer_input", "layer_gemm", "layer_gemm_tf32", "layer_gemm_3xtf32", "layer_output", "layer_score",
- * "layer_score_finalize", "relu_pool".  wino_timing_read() synchronises on the recorded events and
- * returns the summed milliseconds and launch count of one family since the last reset.
+ * "layer_score_finalize", "relu_pool".  Exception: the candidate-chunk launches of one sweep call
+ * ("sweep1d", "sweep2d", "sweep_huffman", "sweep_mixed") form a programmatic-dependent-launch
+ * chain (each chunk may start while the previous drains); the chain is bracketed by ONE event
+ * pair and counts as its number of launches.  wino_timing_read() synchronises on the recorded
+ * events and returns the summed milliseconds and launch count of one family since the last reset.
  * Returns the previous enable state / a wino_status. */
 int wino_timing_enable(int enable);
 void wino_timing_reset(void);

@@ -31,6 +31,7 @@ namespace {
 struct Rec {
   std::string family;
   cudaEvent_t a, b;
+  int count;
 };
 std::mutex g_tmu;
 bool g_timing = false;
@@ -50,9 +51,9 @@ cudaEvent_t timing_event() {
   cudaEventCreate(&e);
   return e;
 }
-void timing_record(const char* family, cudaEvent_t a, cudaEvent_t b) {
+void timing_record(const char* family, cudaEvent_t a, cudaEvent_t b, int count) {
   std::lock_guard<std::mutex> lk(g_tmu);
-  g_recs.push_back(Rec{family, a, b});
+  g_recs.push_back(Rec{family, a, b, count});
 }
 
 }  // namespace wino
@@ -120,7 +121,7 @@ int wino_timing_read(const char* family, double* total_ms, int* launches) {
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, r.a, r.b);
     tot += ms;
-    cnt++;
+    cnt += r.count;
   }
   *total_ms = tot;
   *launches = cnt;

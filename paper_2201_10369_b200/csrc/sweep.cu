@@ -347,7 +347,8 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
 
-  int launches = 0;
+  int launches = 0, chain_len = 0;
+  cudaEvent_t chain_a = nullptr;
   bool refs_done = false;
   MatsParam* P = new MatsParam;
   IdxParam* DI = new IdxParam;
@@ -478,14 +479,37 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     args.n_tgroups = n_tg;
     args.n_cgroups = groups;
     dim3 grid((unsigned)std::min<long long>(n_items, slots));
-    timed_launch(huff ? "sweep_huffman" : mixed ? "sweep_mixed" : dims == 1 ? "sweep1d" : "sweep2d", stream,
-                 [&] { kern<<<grid, kSwThreads, smem, stream>>>(args, *P, *DI); });
+    // PDL chain (sweep_kernels.cuh): every chunk after the call's first may start while the
+    // previous one drains.  With the timing hook on, the chain is timed as ONE interval
+    // (events between its launches would serialise them).
+    if (timing_enabled() && chain_a == nullptr) {
+      chain_a = timing_event();
+      cudaEventRecord(chain_a, stream);
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kSwThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = la;
+    lc.numAttrs = chain_len > 0 ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, args, *P, *DI);
+    chain_len++;
     launches++;
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
       status = set_error(WINO_E_CUDA, "sweep launch: %s", cudaGetErrorString(e));
       break;
     }
+  }
+  if (chain_a != nullptr) {
+    cudaEvent_t chain_b = timing_event();
+    cudaEventRecord(chain_b, stream);
+    timing_record(huff ? "sweep_huffman" : mixed ? "sweep_mixed" : dims == 1 ? "sweep1d" : "sweep2d", chain_a, chain_b,
+                  chain_len);
   }
   if (status == WINO_OK && d_sums != nullptr && n_cand > 0) {
     const double n_out = (double)n_tiles * dy;

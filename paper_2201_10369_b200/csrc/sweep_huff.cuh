@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   u64* slot = slots + tid;
 
+  pdl_launch_dependents();
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_huff_kernel(SweepArgs a, con
       }
     }
   }
+  pdl_wait();
 }
 
 template <int DIMS, int M, int R>

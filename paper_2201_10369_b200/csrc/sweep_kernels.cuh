@@ -48,6 +48,18 @@ struct SweepArgs {
   int n_cgroups;       // candidate groups in this launch; work items = n_cgroups * n_tgroups
 };
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// The candidate chunks of one sweep call are launched as a PDL chain (sweep.cu): chunk k + 1
+// may start as soon as every CTA of chunk k has started (pdl_launch_dependents at entry), so
+// its CTAs fill the SM slots chunk k's last work items leave idle (the wave-quantisation
+// tail of a persistent grid).  The chunks are independent (disjoint candidates and partial
+// rows; the packed tiles / references were written by kernels that completed before the
+// chain's first launch), so no kernel waits before its work; pdl_wait at exit keeps the
+// completion order of the stream (chunk k + 1 completes after chunk k), which the
+// finalize kernel after the chain relies on.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ lane arithmetic
 // Lane<true>: two tiles per thread (FFMA2), Lane<false>: one tile (FFMA).
 // NOFMA (paper arithmetic) uses scalar __fmul_rn/__fadd_rn: ptxas 12.9 contracts
@@ -610,6 +622,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
   double* sacc = reinterpret_cast<double*>(st2 + NN * kSwThreads);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_launch_dependents();
   // persistent CTAs walk the (candidate group, tile group) work items round-robin
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -717,6 +730,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep2d_kernel(SweepArgs a, const 
       for (int f = 0; f < kPartial; f++) pp[f] = v[f];
     }
   }  // work items
+  pdl_wait();
 }
 
 // ------------------------------------------------------------------ K7 (2D, tiles in registers)
@@ -834,6 +848,7 @@ __global__ void __launch_bounds__(kSwThreads, PAIR ? 3 : 1) sweep2d_reg_kernel(S
   const T* gyl = reinterpret_cast<const T*>(a.yl);
 
   const int tid = threadIdx.x;
+  pdl_launch_dependents();
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
@@ -886,6 +901,7 @@ __global__ void __launch_bounds__(kSwThreads, PAIR ? 3 : 1) sweep2d_reg_kernel(S
       ss.write_careful(st, a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial);
     }
   }
+  pdl_wait();
 }
 
 // ------------------------------------------------------------------ K7 (1D)
@@ -965,6 +981,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
   const SmemStats ss = SmemStats::at(smem, reg_cpc_cap(1, true));
 
   const int tid = threadIdx.x;
+  pdl_launch_dependents();
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
@@ -1014,6 +1031,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep1d_kernel(SweepArgs a, const 
       ss.write_careful(st, a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial);
     }
   }
+  pdl_wait();
 }
 
 typedef void (*SweepKernel)(SweepArgs, MatsParam, IdxParam);

@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, co
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* PV = reinterpret_cast<const double*>(P.v);
 
+  pdl_launch_dependents();
   const int n_items = a.n_cgroups * a.n_tgroups;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int cg = item / a.n_tgroups, tg = item - cg * a.n_tgroups;
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(kSwThreads) sweep_mixed_kernel(SweepArgs a, co
       }
     }
   }
+  pdl_wait();
 }
 
 template <int DIMS, int M, int R>

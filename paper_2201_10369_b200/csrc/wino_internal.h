@@ -45,7 +45,9 @@ int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int p
 // ---- kernel timing hook (capi.cpp): when enabled, brackets the launch with cudaEvents
 // on `stream` under the name `family` (read back by wino_timing_read).
 bool timing_enabled();
-void timing_record(const char* family, cudaEvent_t start, cudaEvent_t stop);
+// `count`: launches the (start, stop) pair brackets (a PDL chain of sweep launches is timed
+// as one interval: events between chained launches would serialise them)
+void timing_record(const char* family, cudaEvent_t start, cudaEvent_t stop, int count = 1);
 cudaEvent_t timing_event();
 template <class F>
 void timed_launch(const char* family, cudaStream_t stream, F&& launch) {
