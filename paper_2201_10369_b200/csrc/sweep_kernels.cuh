@@ -60,6 +60,18 @@ struct SweepArgs {
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// ------------------------------------------------------------------ asynchronous staging
+// cp.async of one 4- or 8-byte word global -> shared (LDGSTS: no register round trip, so the
+// copy overlaps the first candidate's arithmetic instead of stalling the warp on the load)
+template <class T>
+__device__ __forceinline__ void cp_async_word(T* dst, const T* src) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "cp.async word");
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(sizeof(T)) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ------------------------------------------------------------------ lane arithmetic
 // Lane<true>: two tiles per thread (FFMA2), Lane<false>: one tile (FFMA).
 // NOFMA (paper arithmetic) uses scalar __fmul_rn/__fadd_rn: ptxas 12.9 contracts
@@ -792,6 +804,8 @@ __device__ __forceinline__ void eval2d_r(const float* __restrict__ cm,
         if (nzA<Z>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
     }
   }
+  // this thread's own y64 slots, staged by cp.async at the tile block's start, have landed
+  if (!CAREFUL) cp_async_wait_all();
 #pragma unroll
   for (int p = 0; p < M; p++) {
 #pragma unroll
@@ -862,14 +876,18 @@ __global__ void __launch_bounds__(kSwThreads, PAIR ? 3 : 1) sweep2d_reg_kernel(S
     __syncthreads();
     for (int tb = tb_begin; tb < tb_end; tb++) {
       const long long tile0 = (long long)tb * TPB;
-      T d[NN], g[RR];
-      load_tiles2d<T, NN, RR>(a, tb, tid, d, g);
-      // each thread stages (and later reads) only its own y64 slots: no barrier needed
+      // each thread stages (and later reads) only its own y64 slots: no barrier needed.  The
+      // copies are asynchronous (waited for before the first scoring) and issued before the
+      // tile loads, so their latency hides behind the first candidate's transforms; the
+      // previous block's reads of these slots were consumed before this point (program order)
 #pragma unroll 4
       for (int o = 0; o < MM; o++) {
-        syh[o * kSwThreads + tid] = __ldg(gyh + ((long long)tb * MM + o) * kSwThreads + tid);
-        syl[o * kSwThreads + tid] = __ldg(gyl + ((long long)tb * MM + o) * kSwThreads + tid);
+        cp_async_word(syh + o * kSwThreads + tid, gyh + ((long long)tb * MM + o) * kSwThreads + tid);
+        cp_async_word(syl + o * kSwThreads + tid, gyl + ((long long)tb * MM + o) * kSwThreads + tid);
       }
+      cp_async_commit();
+      T d[NN], g[RR];
+      load_tiles2d<T, NN, RR>(a, tb, tid, d, g);
       for (int s = c_begin; s < c_end; s++) {
         const float* cm = P.v + s * PER;
         Stat st;
@@ -901,6 +919,7 @@ __global__ void __launch_bounds__(kSwThreads, PAIR ? 3 : 1) sweep2d_reg_kernel(S
       ss.write_careful(st, a.partial + ((long long)DI.idx[s] * a.n_tgroups + tg) * kPartial);
     }
   }
+  cp_async_wait_all();
   pdl_wait();
 }
 
