@@ -193,6 +193,22 @@ int wino_sweep_outputs(int dims, int m, int r, const double* point_sets, int n_c
                        float* d_y, double* d_sums, double* d_maxs, int* cand_status,
                        void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
 
+/* Huffman-order sweeps (WINO_SWEEP_HUFFMAN) run either the shared-memory interpreter
+ * kernel (per-candidate programs in the kernel parameters) or, per class of candidates
+ * with identical per-row Huffman programs, a kernel generated from those programs and
+ * compiled at run time with NVRTC for sm_100a (every tree as straight-line register code;
+ * bit-identical outputs, statistics equal up to fp64 summation order).  mode: 0 = auto
+ * (run-time kernels for sweeps of >= 16384 tiles when NVRTC loads), 1 = always, 2 = never.
+ * Process-wide; returns the previous mode.  Compiled kernels are cached for the process
+ * (wino_huffman_jit_classes() = how many).  A failed compilation in a call that uses them
+ * returns WINO_E_CUDA with NVRTC's log in wino_last_error(). */
+int wino_huffman_jit_mode(int mode);
+int wino_huffman_jit_classes(void);
+/* Diagnostic (host only, no GPU needed): generate and NVRTC-compile the Huffman-order kernel
+ * of the class of one HOST point set [m + r - 1]; *cubin_bytes = the sm_100a cubin size.
+ * Returns WINO_OK, a point-set status, or WINO_E_CUDA (log in wino_last_error()). */
+int wino_huffman_jit_compile_check(int dims, int m, int r, const double* points, size_t* cubin_bytes);
+
 /* Number of kernel launches the last successful call on this thread enqueued
  * (for bench.py's gpu_launches count). */
 int wino_last_launch_count(void);

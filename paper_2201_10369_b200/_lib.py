@@ -38,6 +38,10 @@ SIGNATURES = [
     ("wino_sweep_outputs", ctypes.c_int,
      [ctypes.c_int] * 3 + [_d, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp, _i, _vp, _sz, ctypes.c_uint, _vp]),
     ("wino_last_launch_count", ctypes.c_int, []),
+    ("wino_huffman_jit_mode", ctypes.c_int, [ctypes.c_int]),
+    ("wino_huffman_jit_classes", ctypes.c_int, []),
+    ("wino_huffman_jit_compile_check", ctypes.c_int,
+     [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_size_t)]),
     ("wino_timing_enable", ctypes.c_int, [ctypes.c_int]),
     ("wino_timing_reset", None, []),
     ("wino_timing_read", ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), _i]),

@@ -224,6 +224,27 @@ def wino_last_launch_count() -> int:
     return int(load().wino_last_launch_count())
 
 
+def wino_huffman_jit_mode(mode: int) -> int:
+    """Huffman-order sweep kernels: 0 auto, 1 run-time specialised always, 2 interpreter
+    always (include/wino.h).  Returns the previous mode."""
+    return int(load().wino_huffman_jit_mode(int(mode)))
+
+
+def wino_huffman_jit_classes() -> int:
+    return int(load().wino_huffman_jit_classes())
+
+
+def wino_huffman_jit_compile_check(dims: int, m: int, r: int, points) -> int:
+    """Generate and NVRTC-compile (host only) the Huffman-order kernel of one point set's
+    class; returns the sm_100a cubin size in bytes."""
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    out = ctypes.c_size_t(0)
+    check(load().wino_huffman_jit_compile_check(int(dims), int(m), int(r),
+                                                pts.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(out)),
+          "wino_huffman_jit_compile_check")
+    return int(out.value)
+
+
 def wino_timing_enable(enable: bool) -> bool:
     return bool(load().wino_timing_enable(int(enable)))
 

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "wino_internal.h"
+#include "huff_jit.h"
 
 namespace wino {
 
@@ -92,6 +93,23 @@ const char* wino_status_string(int status) {
 const char* wino_last_error(void) { return g_err; }
 
 int wino_last_launch_count(void) { return g_last_launches; }
+
+int wino_huffman_jit_mode(int mode) { return huff_jit_set_mode(mode < 0 || mode > 2 ? 0 : mode); }
+
+int wino_huffman_jit_classes(void) { return huff_jit_cache_size(); }
+
+int wino_huffman_jit_compile_check(int dims, int m, int r, const double* points, size_t* cubin_bytes) {
+  if (!points || !cubin_bytes) return set_error(WINO_E_INVALID_ARG, "NULL pointer");
+  if (dims < 1 || dims > 2 || m < 1 || r < 1 || m + r - 1 > WINO_MAX_N)
+    return set_error(WINO_E_BAD_SHAPE, "bad shape dims=%d m=%d r=%d", dims, m, r);
+  std::string prog, cubin, log;
+  const int s = huff_class_program(m, r, points, prog);
+  if (s != WINO_OK) return set_error(s, "%s", build_error_detail(s));
+  if (huff_jit_compile(huff_jit_source(dims, m, r, prog), cubin, log) != 0)
+    return set_error(WINO_E_CUDA, "NVRTC: %s", log.substr(0, 900).c_str());
+  *cubin_bytes = cubin.size();
+  return WINO_OK;
+}
 
 int wino_timing_enable(int enable) {
   std::lock_guard<std::mutex> lk(g_tmu);

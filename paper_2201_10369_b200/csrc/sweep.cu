@@ -43,7 +43,10 @@
 //    degenerate-candidate path; padding tiles excluded).  Σ|y64|, max|y64| do not depend
 //    on the candidate and come from K6 (statistics layout, include/wino.h).
 #include <cmath>
+#include <map>
+#include <string>
 
+#include "huff_jit.h"
 #include "sweep_huff.cuh"
 #include "sweep_mixed.cuh"
 
@@ -259,6 +262,30 @@ WsLayout ws_layout(const SweepCfg& c, int n_cand, int64_t n_tiles) {
 
 }  // namespace
 
+int huff_class_program(int m, int r, const double* points, std::string& prog) {
+  const int n = m + r - 1;
+  double AT[WINO_MAX_N * WINO_MAX_N], G[WINO_MAX_N * WINO_MAX_N], BT[WINO_MAX_N * WINO_MAX_N];
+  const int s = build_r64(m, r, points, n, AT, G, BT);
+  if (s != WINO_OK) return s;
+  float row[WINO_MAX_N];
+  prog.assign(huff_prog_bytes(m, r), '\0');
+  unsigned char* pr = reinterpret_cast<unsigned char*>(&prog[0]);
+  // G rows, Bᵀ rows, Aᵀ rows: the record layout of the interpreter's parameters
+  for (int q = 0; q < n; q++, pr += huff_rec_bytes(r)) {
+    for (int j = 0; j < r; j++) row[j] = (float)G[q * r + j];
+    huffman_program(row, r, pr);
+  }
+  for (int q = 0; q < n; q++, pr += huff_rec_bytes(n)) {
+    for (int j = 0; j < n; j++) row[j] = (float)BT[q * n + j];
+    huffman_program(row, n, pr);
+  }
+  for (int q = 0; q < m; q++, pr += huff_rec_bytes(n)) {
+    for (int j = 0; j < n; j++) row[j] = (float)AT[q * n + j];
+    huffman_program(row, n, pr);
+  }
+  return WINO_OK;
+}
+
 int sweep_supported(int dims, int m, int r) { return find_cfg(dims, m, r) != nullptr; }
 
 int sweep_max_cands_per_launch(int dims, int m, int r) {
@@ -287,14 +314,19 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     return set_error(WINO_E_UNSUPPORTED, "no %s sweep kernel for dims=%d m=%d r=%d",
                      huff ? "Huffman-order" : "mixed-precision", dims, m, r);
   const std::vector<Variant>& variants = c->variants;
-  const Family fam = huff ? FAM_HUFF : mixed ? FAM_MIXED
+  const int n = m + r - 1;
+  // Huffman order: run-time specialised register kernels per program class (huff_jit.cu)
+  // for large sweeps, the shared-memory interpreter (sweep_huff.cuh) otherwise; the choice
+  // depends on the mode and the tile count only, never on the candidates (sharding-invariant)
+  const bool jit = huff && huff_jit_wanted(dims, n, n_tiles) && n_tiles > 0 && n_cand > 0;
+  const Family fam = jit ? FAM_SINGLE : huff ? FAM_HUFF : mixed ? FAM_MIXED
                      : c->lay == TPAIR_REG ? FAM_REG : c->lay == TSINGLE_REG ? FAM_REG1
                      : c->lay == TPAIR ? FAM_PAIR : FAM_SINGLE;
   const bool packed = fam == FAM_REG || fam == FAM_REG1;
-  const int n = m + r - 1;
   const int per = per_cand(m, r);
-  // floats per candidate in the params: Huffman = matrices + programs, mixed = fp64 matrices
-  const int stride = huff ? per + huff_prog_words(m, r) : mixed ? 2 * per : per;
+  // floats per candidate in the params: Huffman interpreter = matrices + programs, mixed =
+  // fp64 matrices, Huffman JIT = matrices (the programs are compiled into the kernel)
+  const int stride = huff && !jit ? per + huff_prog_words(m, r) : mixed ? 2 * per : per;
   int cmax = (huff || mixed) ? std::min(kParamFloats / stride, kMaxCandsLaunch)
                              : sweep_max_cands_per_launch(dims, m, r);
   const int dy = dims == 1 ? m : m * m;
@@ -319,7 +351,9 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   double* ref_part = reinterpret_cast<double*>(at(L.ref_part));
   double* ref_tot = reinterpret_cast<double*>(at(L.ref_tot));
   size_t smem = 0;
-  if (huff) {
+  if (jit) {
+    smem = (dims == 2 ? (size_t)n * n * kSwThreads * 4 : 0) + (size_t)kMaxCpc * 4 * kPartial * 8;
+  } else if (huff) {
     smem = (size_t)huff_slot_columns(dims, n) * kSwThreads * 8 + (size_t)dy * 2 * kSwThreads * 8 +
            (size_t)kMaxCpc * 4 * kPartial * 8;
   } else if (mixed) {
@@ -331,9 +365,34 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     const int W = fam == FAM_PAIR ? 2 : 1;
     smem = (size_t)2 * n * n * kSwThreads * 4 * W + (size_t)kMaxCpc * 4 * kPartial * 8;
   }
+  // JIT pre-pass: each accepted candidate's programs -> its class; the classes' kernels
+  // (compiled on first use); candidates processed class by class (order), so every chunk
+  // holds one class
+  std::vector<int> cls(std::max(n_cand, 1), -1), order(std::max(n_cand, 1));
+  for (int k = 0; k < n_cand; k++) order[k] = k;
+  std::vector<const void*> jitk;
+  if (jit) {
+    std::map<std::string, int> ids;
+    std::vector<std::string> progs;
+    std::string prog;
+    for (int k = 0; k < n_cand; k++) {
+      if (huff_class_program(m, r, point_sets + (size_t)k * n, prog) != WINO_OK) continue;
+      auto it = ids.find(prog);
+      if (it == ids.end()) {
+        it = ids.emplace(prog, (int)progs.size()).first;
+        progs.push_back(prog);
+      }
+      cls[k] = it->second;
+    }
+    std::stable_sort(order.begin(), order.begin() + n_cand, [&](int a, int b) { return cls[a] < cls[b]; });
+    std::string err;
+    if (huff_jit_kernels(dims, m, r, progs, jitk, err) != 0) return set_error(WINO_E_CUDA, "%s", err.c_str());
+  }
   if (work && smem > 48 * 1024) {
     std::vector<SweepKernel> ks;
-    if (hc) ks.push_back(hc->k);
+    if (jit)
+      for (const void* k : jitk) ks.push_back(reinterpret_cast<SweepKernel>(const_cast<void*>(k)));
+    else if (hc) ks.push_back(hc->k);
     else
       for (const Variant& v : variants) ks.push_back(v.k[nofma]);
     for (SweepKernel k : ks) {
@@ -368,11 +427,13 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   while (i < n_cand) {
     int nc = 0;
     uint64_t nzA[2] = {0, 0}, nzG[2] = {0, 0}, nzB[2] = {0, 0};   // union over the chunk
-    while (i < n_cand && nc < cmax) {
-      const int s = build_r64(m, r, point_sets + (size_t)i * n, n, AT, G, BT);
-      cand_status[i] = s;
+    const int cur = cls[order[i]];   // JIT: the chunk's class
+    while (i < n_cand && nc < cmax && (!jit || cls[order[i]] == cur)) {
+      const int ci = order[i];
+      const int s = build_r64(m, r, point_sets + (size_t)ci * n, n, AT, G, BT);
+      cand_status[ci] = s;
       if (s == WINO_OK) {
-        ok[i] = 1;
+        ok[ci] = 1;
         float* dst = chunk.data() + (size_t)nc * stride;
         for (int t = 0; t < m * n; t++) {
           dst[t] = (float)AT[t];
@@ -392,7 +453,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
           std::copy(G, G + n * r, d64 + m * n);
           std::copy(BT, BT + n * n, d64 + m * n + n * r);
         }
-        if (huff) {   // programs after the matrices: G rows, Bᵀ rows, Aᵀ rows
+        if (huff && !jit) {   // programs after the matrices: G rows, Bᵀ rows, Aᵀ rows
           unsigned char* pr = reinterpret_cast<unsigned char*>(dst + per);
           std::fill(pr, pr + 4 * huff_prog_words(m, r), (unsigned char)0);
           for (int q = 0; q < n; q++) huffman_program(dst + m * n + q * r, r, pr + q * huff_rec_bytes(r));
@@ -401,7 +462,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
           pr += n * huff_rec_bytes(n);
           for (int q = 0; q < m; q++) huffman_program(dst + q * n, n, pr + q * huff_rec_bytes(n));
         }
-        DI->idx[nc] = i;
+        DI->idx[nc] = ci;
         nc++;
       }
       i++;
@@ -439,12 +500,16 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
         break;
       }
     }
-    SweepKernel kern = hc ? hc->k : var->k[nofma];
+    SweepKernel kern = jit ? reinterpret_cast<SweepKernel>(const_cast<void*>(jitk[cur]))
+                           : hc ? hc->k : var->k[nofma];
     // Work item = (up to cpc candidates, one tile group).  Persistent grid of one wave of
     // resident CTAs walking the items round-robin; cpc is chosen (<= kMaxCpc, larger is
     // better for amortising the tile loads) so the items fill whole rounds of the wave.
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSwThreads, smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSwThreads, smem) != cudaSuccess) {
+      cudaGetLastError();
+      occ = jit ? huff_jit_min_blocks(dims, n) : 1;
+    }
     const long long slots = (long long)std::max(occ, 1) * nsm;
     const int cap = packed ? reg_cpc_cap(dims, fam == FAM_REG) : kMaxCpc;
     int cpc = std::min(cap, nc);

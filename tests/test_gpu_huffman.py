@@ -15,6 +15,16 @@ INF = math.inf
 HUFF = 2
 
 
+@pytest.fixture(autouse=True, params=[2, 1], ids=["interpreter", "jit"])
+def huffman_kernel(request):
+    """Every test runs on both Huffman kernels: the shared-memory interpreter (mode 2) and
+    the run-time specialised register kernels (mode 1, huff_jit.cu)."""
+    from paper_2201_10369_b200 import api
+    prev = api.wino_huffman_jit_mode(request.param)
+    yield request.param
+    api.wino_huffman_jit_mode(prev)
+
+
 def _dev(a):
     import torch
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
@@ -76,6 +86,40 @@ def test_huffman_stats(dims):
     assert np.array_equal(mx, m_ref)                       # fp64 scoring: max exact
     assert np.all(np.abs(s[:, 0] / s_ref[:, 0] - 1) < 1e-12)
     assert np.all(np.abs(s[:, 1] / s_ref[:, 1] - 1) < 1e-12)
+
+
+def test_huffman_jit_classes_compiled(huffman_kernel):
+    """The configs[1] c grid falls into a handful of program classes (8 for F(4,3)); the
+    JIT mode compiles each once and reuses it."""
+    from paper_2201_10369_b200 import api
+    if huffman_kernel != 1:
+        pytest.skip("JIT only")
+    sets = [OP.f43_c(float(c)) for c in synth.c_grid()]
+    d, g = synth.random_tiles(3001, 2, 6, 3, "uniform", seed=3)
+    before = api.wino_huffman_jit_classes()
+    st, s, _ = _stats(2, 4, 3, sets, d, g)
+    mid = api.wino_huffman_jit_classes()
+    st2, s2, _ = _stats(2, 4, 3, sets, d, g)
+    assert np.all(st == 0) and mid - before <= 8 and api.wino_huffman_jit_classes() == mid
+    assert np.array_equal(s, s2)
+    sub = list(range(0, 4096, 511))
+    s_ref, _, _ = ref.sweep(2, 4, 3, [sets[i] for i in sub], d, g, huffman=True)
+    assert np.all(np.abs(s[sub, 0] / s_ref[:, 0] - 1) < 1e-12)
+
+
+def test_huffman_nonfinite_candidates(huffman_kernel):
+    """Overflowing candidates between normal ones: outputs bit-identical (NaN / inf
+    included), exact non-finite counts, neighbours unaffected."""
+    sets = [OP.f43_c(1.3), OP.f43_c(1e19), OP.f43_c(0.7), OP.f43_c(1e-19), OP.f43_c(2.1)]
+    d, g = synth.random_tiles(1003, 2, 6, 3, "uniform", seed=8)
+    st, y = _outputs(2, 4, 3, sets, d, g)
+    _, _, y_ref = ref.sweep(2, 4, 3, sets, d, g, huffman=True, n_dump=d.shape[0])
+    assert np.array_equal(y, y_ref, equal_nan=True)
+    st, s, mx = _stats(2, 4, 3, sets, d, g)
+    s_ref, m_ref, _ = ref.sweep(2, 4, 3, sets, d, g, huffman=True)
+    assert np.array_equal(s[:, 3:], s_ref[:, 3:])
+    fin = s_ref[:, 4] == 0
+    assert np.all(np.abs(s[fin, 0] / s_ref[fin, 0] - 1) < 1e-12)
 
 
 @pytest.mark.parametrize("dims", [1, 2])

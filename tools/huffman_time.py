@@ -19,7 +19,8 @@ for dims in (1, 2):
     dd, gg = torch.from_numpy(d).cuda(), torch.from_numpy(g).cuda()
     S, T = len(sets), d.shape[0]
     ws = torch.empty(api.wino_error_sweep_workspace_bytes(dims, 4, 3, S, T), dtype=torch.uint8, device="cuda")
-    for name, flags in (("fma", 0), ("nofma", 1), ("huffman", 2), ("mixed", 4)):
+    for name, flags, jit in (("fma", 0, 0), ("nofma", 1, 0), ("huffman", 2, 1), ("huffman_interp", 2, 2), ("mixed", 4, 0)):
+        api.wino_huffman_jit_mode(jit)
         sums = torch.zeros((S, 5), dtype=torch.float64, device="cuda")
         maxs = torch.zeros((S, 2), dtype=torch.float64, device="cuda")
         api.wino_error_sweep(dims, 4, 3, sets, dd, gg, sums, maxs, ws, flags=flags)
