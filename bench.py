@@ -134,6 +134,17 @@ def _flops_per_tile_eval(dims, m, r, AT, G, BT):
     return 2 * fma + mul, fma, dense, mul
 
 
+def _huffman_ops_per_tile_eval(m, r, AT, G, BT):
+    """Huffman-order 2D tile evaluation (reading R21): one FMUL per non-zero coefficient use
+    (the FMA count of _flops_per_tile_eval) and per Hadamard element, one FADD per tree node
+    = uses minus the non-empty dot products.  Every op is one FP32-pipe lane-op."""
+    n = m + r - 1
+    rows = lambda M: int(np.count_nonzero(np.any(M != 0, axis=1)))
+    _, fma, _, mul = _flops_per_tile_eval(2, m, r, AT, G, BT)
+    dots = (r + n) * rows(G) + 2 * n * rows(BT) + (n + m) * rows(AT)
+    return fma + mul + (fma - dots)
+
+
 # ------------------------------------------------------------------ reference arm / cpu baseline
 
 def oracle_sample_run(specs, every: int):
@@ -553,6 +564,17 @@ def main():
                 "workload": f"configs[1] 2D {sp.spec.dist} sweep ({S} c x {T} tiles), {note}",
                 "ms": hms, "ms_runs": runs, "value": S * T / (hms * 1e-3), "unit": "tile-evals/s",
                 "argmin_c": float(sp.spec.params[i]) if i is not None else None, "min_mae": best}
+            if vname == "huffman_2d":
+                ops = _huffman_ops_per_tile_eval(4, 3, AT, G, BT)
+                nsm_ = torch.cuda.get_device_properties(dev).multi_processor_count
+                alu_peak = nsm_ * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+                ach = S * T * ops / (hms * 1e-3) / 1e12
+                variants[vname]["kernel"] = ("run-time specialised register kernels, one per Huffman program class "
+                                             "(NVRTC, huff_jit.cu); auto mode")
+                variants[vname]["roofline"] = {
+                    "bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "Top/s", "frac": ach / alu_peak,
+                    "fp32_ops_per_tile_eval": ops,
+                    "peak_source": f"{nsm_} SMs x 128 FP32 lanes x 1 op (unfused FMUL / FADD) x sm_max_mhz"}
             if vname == "mixed_2d":
                 # dense fp64 transforms: 2D F(4x4,3x3) = 6*3*3 + 6*6*3 + 6*6*6*2 + 4*6*6 + 4*4*6 DFMA
                 dfma = 6 * 3 * 3 + 6 * 6 * 3 + 2 * 6 * 6 * 6 + 4 * 6 * 6 + 4 * 4 * 6

@@ -12,7 +12,9 @@
 #include <dlfcn.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -207,6 +209,13 @@ std::string huff_jit_source(int dims, int m, int r, const std::string& prog) {
 }
 
 int huff_jit_compile(const std::string& src, std::string& cubin, std::string& log) {
+  if (const char* dir = std::getenv("WINO_JIT_DUMP")) {   // inspection: nvcc -Xptxas -v, cuobjdump
+    const std::string base = std::string(dir) + "/huffjit_" + std::to_string(std::hash<std::string>()(src));
+    if (FILE* f = std::fopen((base + ".cu").c_str(), "w")) {
+      std::fputs(src.c_str(), f);
+      std::fclose(f);
+    }
+  }
   const Nvrtc& nv = nvrtc();
   if (!nv.ok) {
     log = nv.why;

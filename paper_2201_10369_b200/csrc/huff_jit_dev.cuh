@@ -85,12 +85,23 @@ __device__ __forceinline__ void huff_jit_run(const SweepArgs& a, const MatsParam
 #pragma unroll
           for (int o = 0; o < DY; o++) yd[o] = y[o];
         }
+        // fast path: unconditional fp64 scoring (a padding tile has y = y64 = 0: no effect);
+        // if any sum of the warp went non-finite, the same outputs are re-scored exactly with
+        // per-output finiteness and padding tiles excluded (Stat::add_careful)
         Stat st;
-        if (ok) {
 #pragma unroll
-          for (int o = 0; o < DY; o++) {
-            if (o & 1) st.add_careful<1>(y[o], __ldg(yt + o * kSwThreads));
-            else st.add_careful<0>(y[o], __ldg(yt + o * kSwThreads));
+        for (int o = 0; o < DY; o++) {
+          if (o & 1) st.add_fast<1>(y[o], __ldg(yt + o * kSwThreads));
+          else st.add_fast<0>(y[o], __ldg(yt + o * kSwThreads));
+        }
+        if (__any_sync(0xffffffffu, !st.finite())) {
+          st = Stat();
+          if (ok) {
+#pragma unroll
+            for (int o = 0; o < DY; o++) {
+              if (o & 1) st.add_careful<1>(y[o], __ldg(yt + o * kSwThreads));
+              else st.add_careful<0>(y[o], __ldg(yt + o * kSwThreads));
+            }
           }
         }
         st.warp_reduce();

@@ -423,8 +423,16 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
   constexpr int W = L::W;
   constexpr int N = M + R - 1, MM = M * M;
   constexpr int OFF_G = M * N, OFF_B = M * N + N * R;
+  // COMPACT (n >= 9): the column loop of T2 and the row loop of U / V / T3 are NOT unrolled.
+  // Fully unrolled, one F(6x6,5x5) evaluation is ~3000 FFMAs (150 KB of SASS with the careful
+  // path) and the warps stall on instruction fetch (ncu: "no instructions" the top stall).
+  // Rolled, the hot code shrinks ~10x.  The structural zeros of Bᵀ (T2, V) and G (U) depend
+  // only on the unrolled indices and stay compile-time skipped; T1 = G g and the T3 update
+  // (whose zeros depend on the rolled row i) run dense -- the canonical chains themselves
+  // (parity semantics: skipping a zero term is the optimisation, not the definition).
+  constexpr bool COMPACT = N >= 9;
   // T2 = Bᵀ d, column by column (d column q from smem), staged to smem
-#pragma unroll
+#pragma unroll (COMPACT ? 1 : N)
   for (int q = 0; q < N; q++) {
     T dc[N];
 #pragma unroll
@@ -443,7 +451,7 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
   for (int p = 0; p < M; p++)
 #pragma unroll
     for (int l = 0; l < N; l++) t3[p][l] = L::zero();
-#pragma unroll
+#pragma unroll (COMPACT ? 1 : N)
   for (int i = 0; i < N; i++) {
     // U row i = (G g Gᵀ)[i,:]:  T1[i][q] = Σ_j G[i][j] g[j][q];  U[i][l] = Σ_q T1[i][q] G[l][q]
     T t1[R];
@@ -452,7 +460,7 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       T acc = L::zero();
 #pragma unroll
       for (int j = 0; j < R; j++)
-        if (nzG<Z>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
+        if (COMPACT || nzG<Z>(i * R + j)) acc = L::fma(g[j * R + q], cm[OFF_G + i * R + j], acc);
       t1[q] = acc;
     }
     T t2r[N];
@@ -473,7 +481,7 @@ __device__ __forceinline__ void eval2d(const float* __restrict__ cm, const typen
       // T3[p][l] += Aᵀ[p][i] Mw[i][l]  (ascending i, from +0)
 #pragma unroll
       for (int p = 0; p < M; p++)
-        if (nzA<Z>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
+        if (COMPACT || nzA<Z>(p * N + i)) t3[p][l] = L::fma(mw, cm[p * N + i], t3[p][l]);
     }
   }
   // Y[p][q] = Σ_l T3[p][l] Aᵀ[q][l]; score (and write)

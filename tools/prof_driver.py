@@ -46,6 +46,18 @@ def main():
         pts = PP.family_n8_cd(2.0, 1.003)
         y, s, mx = api.conv2d(xd, wd, pad, m, pts, score=True)
         torch.cuda.synchronize()
+    if what == "huff":    # configs[1] 2D uniform Huffman-order sweep, run-time specialised kernels
+        sets = np.array([PP.family_f43(float(c)) for c in synth.c_grid(4096)])
+        d, g = synth.random_tiles(100_000, 2, 6, 3, "uniform", 0)
+        dd, gg = torch.from_numpy(d).to(dev), torch.from_numpy(g).to(dev)
+        S, T = len(sets), d.shape[0]
+        ws = torch.empty(api.wino_error_sweep_workspace_bytes(2, 4, 3, S, T), dtype=torch.uint8, device=dev)
+        sums = torch.zeros((S, 5), dtype=torch.float64, device=dev)
+        maxs = torch.zeros((S, 2), dtype=torch.float64, device=dev)
+        api.wino_huffman_jit_mode(1)
+        for _ in range(2):
+            api.wino_error_sweep(2, 4, 3, sets, dd, gg, sums, maxs, ws, flags=api.WINO_SWEEP_HUFFMAN)
+        torch.cuda.synchronize()
     if what in ("all", "layer"):
         N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
         x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
