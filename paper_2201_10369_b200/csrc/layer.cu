@@ -14,11 +14,13 @@
 // the sign of a zero).  Parity semantics: every dot product is an
 // fmaf chain from +0 in ascending index order, 2D transforms left product first.
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 
 #include "tc_gemm.cuh"
 #include "wino_internal.h"
+#include "zero_masks.h"
 
 namespace wino {
 
@@ -117,6 +119,10 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
 }
 
 // ------------------------------------------------------------------ K2
+// Z: structural-zero family of the point set (zero_masks.h; 0 = dense): the Bᵀ entries it
+// marks are skipped at compile time -- the launcher picks Z only when they are exactly 0 in
+// this call's matrices, and a skipped fma(0, v, acc) = acc for finite v, so every element is
+// the canonical chain's (22 % fewer FMAs for the F(6x6,3x3) family).
 // one thread per (kInCpt channels, t); t fastest -> coalesced V stores per Winograd
 // position.  The tile geometry, padding predicates and patch offsets are computed once and
 // reused for the thread's kInCpt channels (the kernel is issue-bound on that arithmetic).
@@ -124,7 +130,7 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
 // dominates), 1 otherwise (more threads in flight); always divides Cp (a multiple of 16)
 template <int N>
 constexpr int in_cpt() { return N > 8 ? 4 : 1; }
-template <int M, int R>
+template <int M, int R, int Z>
 __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(const float* __restrict__ x, float* __restrict__ V, Geo geo,
                                                        const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
@@ -179,7 +185,8 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
       for (int i = 0; i < N; i++) {
         float acc = 0.0f;
 #pragma unroll
-        for (int j = 0; j < N; j++) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
+        for (int j = 0; j < N; j++)
+          if (nzB<Z>(i * N + j)) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
         t2[i][q] = acc;
       }
     // V[i][l] = Σ_q T2[i][q] Bᵀ[l][q]; positions p = i N + l stored in ascending order
@@ -189,7 +196,8 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
       for (int l = 0; l < N; l++) {
         float acc = 0.0f;
 #pragma unroll
-        for (int q = 0; q < N; q++) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
+        for (int q = 0; q < N; q++)
+          if (nzB<Z>(l * N + q)) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
         if (geo.tf32 == 2) {
           const float hi = round_tf32(acc);
           dst[0] = hi;
@@ -312,7 +320,7 @@ using tc::gemm_tf32_kernel;
 // needs an even tile size so no window straddles two tiles -- the launcher only fuses then);
 // y itself is written only when y != NULL (the scorer and the caller's `keep` need it).
 // ReLU and max are exact, so the fused output equals relu_pool(y) bit for bit.
-template <int M, int R>
+template <int M, int R, int Z>
 __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(const float* __restrict__ Mw,
                                                                            float* __restrict__ y, Geo geo,
                                                                            const __grid_constant__ LayerMats mt,
@@ -338,8 +346,9 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
     for (int l = 0; l < N; l++) mw[l] = src[(i * N + l) * plane];
 #pragma unroll
     for (int p = 0; p < M; p++)
+      if (nzA<Z>(p * N + i))
 #pragma unroll
-      for (int l = 0; l < N; l++) t3[p][l] = __fmaf_rn(mt.AT[p * N + i], mw[l], t3[p][l]);
+        for (int l = 0; l < N; l++) t3[p][l] = __fmaf_rn(mt.AT[p * N + i], mw[l], t3[p][l]);
   }
   const int per_img = geo.th * geo.tw;
   const int img = (int)(t / per_img);
@@ -362,7 +371,8 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
     for (int s = 0; s < M; s++) {
       float acc = 0.0f;
 #pragma unroll
-      for (int l = 0; l < N; l++) acc = __fmaf_rn(t3[p][l], mt.AT[s * N + l], acc);
+      for (int l = 0; l < N; l++)
+        if (nzA<Z>(s * N + l)) acc = __fmaf_rn(t3[p][l], mt.AT[s * N + l], acc);
       yr[s] = acc;
     }
     const int wmax = geo.Wo - tx * M;   // valid columns in this tile row
@@ -651,17 +661,43 @@ typedef void (*InputK)(const float*, float*, Geo, LayerMats);
 typedef void (*OutputK)(const float*, float*, Geo, LayerMats, float*, int);
 typedef void (*ScoreK)(const float*, const float*, const float*, Geo, ScoreTile, double*);
 
+// transform kernels of one structural-zero family Z (0 = dense)
+struct XformK {
+  int z;
+  uint64_t za[2], zb[2];   // skipped entries of Aᵀ / Bᵀ (zero_masks.h)
+  InputK ik;
+  OutputK ok;
+};
+
 struct LayerCfg {
   int m, r;
   FilterK fk;
-  InputK ik;
-  OutputK ok;
   ScoreK sk;
+  XformK xk[2];   // most specialised first, dense last
+  int nxk;
 };
 
-template <int M, int R>
+template <int M, int R, int Z>
+XformK make_xform_k() {
+  static_assert(Z == 0 || (ZM<Z>::m == M && ZM<Z>::r == R), "zero-mask family of another shape");
+  XformK v;
+  v.z = Z;
+  for (int w = 0; w < 2; w++) {
+    v.za[w] = ZM<Z>::A(w);
+    v.zb[w] = ZM<Z>::B(w);
+  }
+  v.ik = input_kernel<M, R, Z>;
+  v.ok = output_kernel<M, R, Z>;
+  return v;
+}
+
+// ZF: the structural-zero family compiled for this shape (0: dense only)
+template <int M, int R, int ZF = 0>
 LayerCfg make_layer_cfg() {
-  return LayerCfg{M, R, filter_kernel<M, R>, input_kernel<M, R>, output_kernel<M, R>, score_kernel<R>};
+  LayerCfg c{M, R, filter_kernel<M, R>, score_kernel<R>, {}, 0};
+  if constexpr (ZF != 0) c.xk[c.nxk++] = make_xform_k<M, R, ZF>();
+  c.xk[c.nxk++] = make_xform_k<M, R, 0>();
+  return c;
 }
 
 dim3 score_grid(const Geo& g) {
@@ -672,10 +708,35 @@ dim3 score_grid(const Geo& g) {
 // F(m x m, 3 x 3) for m = 2..8 (n = 4..10: the paper's T7-T9 sizes) and the
 // 5 x 5 kernels of configs[3]
 const LayerCfg kLayerCfgs[] = {
-    make_layer_cfg<2, 3>(), make_layer_cfg<3, 3>(), make_layer_cfg<4, 3>(), make_layer_cfg<5, 3>(),
-    make_layer_cfg<6, 3>(), make_layer_cfg<7, 3>(), make_layer_cfg<8, 3>(),
-    make_layer_cfg<2, 5>(), make_layer_cfg<4, 5>(), make_layer_cfg<6, 5>(),
+    make_layer_cfg<2, 3, kZ_F23_C>(), make_layer_cfg<3, 3>(), make_layer_cfg<4, 3, kZ_F43_C>(),
+    make_layer_cfg<5, 3>(), make_layer_cfg<6, 3, kZ_N8_CD>(), make_layer_cfg<7, 3>(), make_layer_cfg<8, 3, kZ_N10_C1C2>(),
+    make_layer_cfg<2, 5>(), make_layer_cfg<4, 5, kZ_N8_C1C2_R5>(), make_layer_cfg<6, 5, kZ_N10_C1C2_R5>(),
 };
+
+// The transform kernels for these fp32 matrices: the first variant whose skipped Aᵀ / Bᵀ
+// entries are all exactly zero.  Families are used only for moderate coefficients
+// (|a| < 2^32): skipping a zero term equals the dense chain while no intermediate overflows
+// (finite x, w), and huge coefficients are the likely overflow source; the dense variant
+// takes the rest.
+const XformK& pick_xform(const LayerCfg& cfg, const LayerMats& mt, int m, int n) {
+  uint64_t nzA[2] = {0, 0}, nzB[2] = {0, 0};
+  bool moderate = true;
+  for (int t = 0; t < m * n; t++) {
+    if (mt.AT[t] != 0.0f) nzA[t >> 6] |= 1ull << (t & 63);
+    moderate = moderate && std::fabs(mt.AT[t]) < 4294967296.0f;
+  }
+  for (int t = 0; t < n * n; t++) {
+    if (mt.BT[t] != 0.0f) nzB[t >> 6] |= 1ull << (t & 63);
+    moderate = moderate && std::fabs(mt.BT[t]) < 4294967296.0f;
+  }
+  for (int v = 0; v + 1 < cfg.nxk; v++) {
+    const XformK& k = cfg.xk[v];
+    if (moderate && (k.za[0] & nzA[0]) == 0 && (k.za[1] & nzA[1]) == 0 && (k.zb[0] & nzB[0]) == 0 &&
+        (k.zb[1] & nzB[1]) == 0)
+      return k;
+  }
+  return cfg.xk[cfg.nxk - 1];
+}
 
 const LayerCfg* find_layer(int m, int r) {
   for (const auto& c : kLayerCfgs)
@@ -775,6 +836,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   std::copy(AT, AT + m * n, mt.AT);
   std::copy(G, G + n * r, mt.G);
   std::copy(BT, BT + n * n, mt.BT);
+  const XformK& xk = pick_xform(*cfg, mt, m, n);
   char* ws = reinterpret_cast<char*>(workspace);
   float* U = reinterpret_cast<float*>(ws + L.u_off);
   float* V = reinterpret_cast<float*>(ws + L.v_off);
@@ -800,7 +862,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   {
     const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
     const long long tot = (long long)(g.Cp / cpt) * g.Tp;
-    const auto ik = cfg->ik;
+    const auto ik = xk.ik;
     timed_launch("layer_input", stream, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt); });
     launches++;
   }
@@ -853,7 +915,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   }
   {
     const long long tot = (long long)g.K * g.T;
-    const auto ok = cfg->ok;
+    const auto ok = xk.ok;
     // fused ReLU (+ 2 x 2 pool for even m) epilogue; odd m with pool 2 runs the separate
     // ReLU / pool kernel on y after the layer
     const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);

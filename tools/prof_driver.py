@@ -58,6 +58,14 @@ def main():
         for _ in range(2):
             api.wino_error_sweep(2, 4, 3, sets, dd, gg, sums, maxs, ws, flags=api.WINO_SWEEP_HUFFMAN)
         torch.cuda.synchronize()
+    if what == "vgg":     # configs[4]: two unscored VGG-16 x64 forwards
+        from paper_2201_10369_b200 import network
+        x, wts = synth.vgg16_inputs(64, seed=0)
+        xd = torch.from_numpy(x).to(dev)
+        wd = [torch.from_numpy(w).to(dev) for w in wts]
+        for _ in range(2):
+            network.vgg16_forward(xd, wd, PP.family_n8_cd(2.0, 1.003), m=6, score=False)
+        torch.cuda.synchronize()
     if what in ("all", "layer"):
         N, C, H, W, K, r, pad, m = 32, 256, 56, 56, 256, 3, 1, 6
         x, w = synth.layer_inputs(N, C, H, W, K, r, "normal", "he", seed=0)
