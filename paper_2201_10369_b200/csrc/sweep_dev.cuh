@@ -13,7 +13,7 @@ constexpr int kParamFloats = 7424;     // coefficient floats per launch (29696 B
 constexpr int kMaxCandsLaunch = 512;   // + 2 KB of candidate indices: < 32764 B of params
 constexpr int kMaxCpc = 32;            // candidates per CTA work item (<= 32: flag ballot)
 constexpr int kPartial = 4;            // doubles per partial: s0, s1, m0, nonfin
-constexpr int kKP1 = 4;                // 1D: tile pairs per thread and tile block
+constexpr int kKP1 = 2;                // 1D: tile pairs per thread and tile block
 constexpr int kGroupTiles = 2 * kSwThreads;   // tiles per packed group (one pair per thread)
 
 struct __align__(16) MatsParam {
