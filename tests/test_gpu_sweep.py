@@ -115,6 +115,10 @@ def test_f43_stats(dims, dist):
     (1, 6, 5, OP.n10_c1c2, [(1.272, 2.099)]),
     (2, 8, 3, OP.n10_c1c2, [(1.272, 2.099)]),
     (1, 8, 3, OP.n10_c1c2, [(1.953, 1.229)]),
+    # dense (no structural-zero family) large-n kernels with the rolled loops (COMPACT, n >= 9)
+    (2, 7, 3, OP.chebyshev, [9]),
+    (2, 6, 5, OP.chebyshev, [10]),
+    (2, 8, 3, OP.chebyshev, [10]),
 ])
 def test_other_templates_bitexact(dims, m, r, maker, args):
     sets = [maker(*(a if isinstance(a, tuple) else (a,))) for a in args]
