@@ -18,8 +18,9 @@ Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on
 launching stream, the L2 flushed (512 MB write) between steps outside the events;
 barrier + synchronize around the timed region; max over ranks.  Clocks are sampled with
 NVML during the timed region.  `e2e` repeats the job through the same C-ABI call with the
-tiles copied H2D from pinned host memory and the statistics copied back D2H inside the
-timed region.  `cpu_baseline` / `--impl reference` time the oracle (oracle/, plain C,
+tiles copied H2D from pinned host memory (on a copy stream, each sweep waiting for its own
+tiles, so later sweeps' copies overlap earlier sweeps' kernels) and the statistics copied
+back D2H inside the timed region.  `cpu_baseline` / `--impl reference` time the oracle (oracle/, plain C,
 OpenMP) on the host cores on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -486,26 +487,46 @@ def main():
     h2d = sum(p[0].numel() * 4 + p[1].numel() * 4 for p in pinned)
     d2h = sum(o[0].numel() * 8 + o[1].numel() * 8 for o in out_host)
     e2e_ms, e2e_copy_ms, host_ms = [], [], []
+    # The copies run on a side stream, one event per sweep: sweep k waits only for its own
+    # tiles, so sweep k + 1's H2D overlaps sweep k's kernels (every copy is still inside the
+    # timed region, which ends after the D2H of the statistics).  Both streams are created
+    # streams: work on the legacy default stream would serialise with every copy.
+    from paper_2201_10369_b200.sweep import abi_compute
+    copy_stream = torch.cuda.Stream(device=dev)
+    comp = torch.cuda.Stream(device=dev)
     barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
-        flush()
-        a, c, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        a.record(stream)
-        for rs, (pd, pg) in zip(rsw, pinned):
-            rs.d_tiles.copy_(pd, non_blocking=True)
-            rs.g_tiles.copy_(pg, non_blocking=True)
-        c.record(stream)
-        h0 = time.perf_counter()
-        run_step(rsw)
-        host_ms.append(1e3 * (time.perf_counter() - h0))
-        for rs, (hs, hm) in zip(rsw, out_host):
-            hs.copy_(rs.sums, non_blocking=True)
-            hm.copy_(rs.maxs, non_blocking=True)
-        b.record(stream)
+        with torch.cuda.stream(comp):
+            flush()
+            a, c, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            ready = {}
+            a.record(comp)
+            copy_stream.wait_stream(comp)
+            with torch.cuda.stream(copy_stream):
+                for rs, (pd, pg) in zip(rsw, pinned):
+                    rs.d_tiles.copy_(pd, non_blocking=True)
+                    rs.g_tiles.copy_(pg, non_blocking=True)
+                    ready[id(rs)] = torch.cuda.Event()
+                    ready[id(rs)].record(copy_stream)
+                c.record(copy_stream)
+
+            def compute_after_copy(rs):
+                comp.wait_event(ready[id(rs)])
+                abi_compute(rs)   # on the current stream = comp
+
+            h0 = time.perf_counter()
+            run_step(rsw, compute=compute_after_copy)
+            host_ms.append(1e3 * (time.perf_counter() - h0))
+            comp.wait_event(c)   # (already implied by the last sweep's wait; keeps the region closed)
+            for rs, (hs, hm) in zip(rsw, out_host):
+                hs.copy_(rs.sums, non_blocking=True)
+                hm.copy_(rs.maxs, non_blocking=True)
+            b.record(comp)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
         e2e_copy_ms.append(a.elapsed_time(c))
+    torch.cuda.synchronize()
     e2e_tot = sum(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)

@@ -42,7 +42,10 @@
 //    non-finite; such a candidate is re-evaluated with per-output checks (the rare
 //    degenerate-candidate path; padding tiles excluded).  Σ|y64|, max|y64| do not depend
 //    on the candidate and come from K6 (statistics layout, include/wino.h).
+#include <chrono>
+#include <omp.h>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <string>
 
@@ -411,11 +414,21 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   bool refs_done = false;
   MatsParam* P = new MatsParam;
   IdxParam* DI = new IdxParam;
-  std::vector<float> chunk((size_t)cmax * stride);
+  std::vector<float> chunk((size_t)cmax * stride);   // per chunk position
+  std::vector<int> pos_status(cmax);
+  std::vector<uint64_t> pos_nz((size_t)cmax * 6);
   std::vector<int> ok(std::max(n_cand, 1), 0);
-  double AT[WINO_MAX_N * WINO_MAX_N], G[WINO_MAX_N * WINO_MAX_N], BT[WINO_MAX_N * WINO_MAX_N];
+  const int build_threads = std::max(1, std::min(8, omp_get_max_threads()));
   int i = 0;
   int status = WINO_OK;
+  // WINO_HOST_PROFILE=1: per call, the host time spent building matrices, choosing the
+  // launch shape and enqueueing (stderr) -- the enqueue rate bounds short launches
+  static const bool host_prof = std::getenv("WINO_HOST_PROFILE") != nullptr;
+  double t_build = 0.0, t_occ = 0.0, t_launch = 0.0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto since = [](std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  };
   // non-zero positions of one fp32 matrix as a 128-bit mask; an entry beyond bit 127
   // saturates both words ("nothing may be skipped": only the dense variant matches)
   auto mark = [](uint64_t (&nz)[2], int t) {
@@ -425,50 +438,66 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   // Matrices are built chunk by chunk (a2 on the host) while the previous chunk's kernels
   // run: launches are asynchronous, so host construction overlaps device work.
   while (i < n_cand) {
+    const auto tb0 = now();
     int nc = 0;
     uint64_t nzA[2] = {0, 0}, nzG[2] = {0, 0}, nzB[2] = {0, 0};   // union over the chunk
     const int cur = cls[order[i]];   // JIT: the chunk's class
-    while (i < n_cand && nc < cmax && (!jit || cls[order[i]] == cur)) {
-      const int ci = order[i];
+    // the chunk's positions: up to cmax candidates in processing order (one class for JIT)
+    int L = 0;
+    while (i + L < n_cand && L < cmax && (!jit || cls[order[i + L]] == cur)) L++;
+    // build them in parallel host threads (R64 per candidate is independent and
+    // deterministic), then compact the accepted ones into the kernel parameters
+#pragma omp parallel for schedule(static) num_threads(build_threads) if (L >= 64)
+    for (int k = 0; k < L; k++) {
+      const int ci = order[i + k];
+      double AT[WINO_MAX_N * WINO_MAX_N], G[WINO_MAX_N * WINO_MAX_N], BT[WINO_MAX_N * WINO_MAX_N];
       const int s = build_r64(m, r, point_sets + (size_t)ci * n, n, AT, G, BT);
-      cand_status[ci] = s;
-      if (s == WINO_OK) {
-        ok[ci] = 1;
-        float* dst = chunk.data() + (size_t)nc * stride;
-        for (int t = 0; t < m * n; t++) {
-          dst[t] = (float)AT[t];
-          if (dst[t] != 0.0f) mark(nzA, t);
-        }
-        for (int t = 0; t < n * r; t++) {
-          dst[m * n + t] = (float)G[t];
-          if (dst[m * n + t] != 0.0f) mark(nzG, t);
-        }
-        for (int t = 0; t < n * n; t++) {
-          dst[m * n + n * r + t] = (float)BT[t];
-          if (dst[m * n + n * r + t] != 0.0f) mark(nzB, t);
-        }
-        if (mixed) {   // the fp64 matrices themselves (R64, not rounded)
-          double* d64 = reinterpret_cast<double*>(dst);
-          std::copy(AT, AT + m * n, d64);
-          std::copy(G, G + n * r, d64 + m * n);
-          std::copy(BT, BT + n * n, d64 + m * n + n * r);
-        }
-        if (huff && !jit) {   // programs after the matrices: G rows, Bᵀ rows, Aᵀ rows
-          unsigned char* pr = reinterpret_cast<unsigned char*>(dst + per);
-          std::fill(pr, pr + 4 * huff_prog_words(m, r), (unsigned char)0);
-          for (int q = 0; q < n; q++) huffman_program(dst + m * n + q * r, r, pr + q * huff_rec_bytes(r));
-          pr += n * huff_rec_bytes(r);
-          for (int q = 0; q < n; q++) huffman_program(dst + m * n + n * r + q * n, n, pr + q * huff_rec_bytes(n));
-          pr += n * huff_rec_bytes(n);
-          for (int q = 0; q < m; q++) huffman_program(dst + q * n, n, pr + q * huff_rec_bytes(n));
-        }
-        DI->idx[nc] = ci;
-        nc++;
+      pos_status[k] = s;
+      uint64_t* nz = pos_nz.data() + (size_t)k * 6;
+      for (int w = 0; w < 6; w++) nz[w] = 0;
+      if (s != WINO_OK) continue;
+      float* dst = chunk.data() + (size_t)k * stride;
+      for (int t = 0; t < m * n; t++) {
+        dst[t] = (float)AT[t];
+        if (dst[t] != 0.0f) mark(*reinterpret_cast<uint64_t(*)[2]>(nz + 0), t);
       }
-      i++;
+      for (int t = 0; t < n * r; t++) {
+        dst[m * n + t] = (float)G[t];
+        if (dst[m * n + t] != 0.0f) mark(*reinterpret_cast<uint64_t(*)[2]>(nz + 2), t);
+      }
+      for (int t = 0; t < n * n; t++) {
+        dst[m * n + n * r + t] = (float)BT[t];
+        if (dst[m * n + n * r + t] != 0.0f) mark(*reinterpret_cast<uint64_t(*)[2]>(nz + 4), t);
+      }
+      if (mixed) {   // the fp64 matrices themselves (R64, not rounded)
+        double* d64 = reinterpret_cast<double*>(dst);
+        std::copy(AT, AT + m * n, d64);
+        std::copy(G, G + n * r, d64 + m * n);
+        std::copy(BT, BT + n * n, d64 + m * n + n * r);
+      }
+      if (huff && !jit) {   // programs after the matrices: G rows, Bᵀ rows, Aᵀ rows
+        unsigned char* pr = reinterpret_cast<unsigned char*>(dst + per);
+        std::fill(pr, pr + 4 * huff_prog_words(m, r), (unsigned char)0);
+        for (int q = 0; q < n; q++) huffman_program(dst + m * n + q * r, r, pr + q * huff_rec_bytes(r));
+        pr += n * huff_rec_bytes(r);
+        for (int q = 0; q < n; q++) huffman_program(dst + m * n + n * r + q * n, n, pr + q * huff_rec_bytes(n));
+        pr += n * huff_rec_bytes(n);
+        for (int q = 0; q < m; q++) huffman_program(dst + q * n, n, pr + q * huff_rec_bytes(n));
+      }
     }
+    for (int k = 0; k < L; k++) {
+      const int ci = order[i + k];
+      cand_status[ci] = pos_status[k];
+      if (pos_status[k] != WINO_OK) continue;
+      ok[ci] = 1;
+      const uint64_t* nz = pos_nz.data() + (size_t)k * 6;
+      nzA[0] |= nz[0], nzA[1] |= nz[1], nzG[0] |= nz[2], nzG[1] |= nz[3], nzB[0] |= nz[4], nzB[1] |= nz[5];
+      std::copy(chunk.data() + (size_t)k * stride, chunk.data() + (size_t)(k + 1) * stride, P->v + (size_t)nc * stride);
+      DI->idx[nc] = ci;
+      nc++;
+    }
+    i += L;
     if (nc == 0 || n_tiles <= 0) continue;
-    std::copy(chunk.data(), chunk.data() + (size_t)nc * stride, P->v);
     if (!refs_done) {
       if (packed) {
         const auto prep = c->prep;
@@ -502,6 +531,8 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     }
     SweepKernel kern = jit ? reinterpret_cast<SweepKernel>(const_cast<void*>(jitk[cur]))
                            : hc ? hc->k : var->k[nofma];
+    t_build += since(tb0);
+    const auto to0 = now();
     // Work item = (up to cpc candidates, one tile group).  Persistent grid of one wave of
     // resident CTAs walking the items round-robin; cpc is chosen (<= kMaxCpc, larger is
     // better for amortising the tile loads) so the items fill whole rounds of the wave.
@@ -525,6 +556,8 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     }
     const int groups = (nc + cpc - 1) / cpc;
     const long long n_items = (long long)groups * n_tg;
+    t_occ += since(to0);
+    const auto tl0 = now();
     SweepArgs args;
     args.d = d_tiles;
     args.g = g_tiles;
@@ -565,6 +598,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
     chain_len++;
     launches++;
     if (e == cudaSuccess) e = cudaGetLastError();
+    t_launch += since(tl0);
     if (e != cudaSuccess) {
       status = set_error(WINO_E_CUDA, "sweep launch: %s", cudaGetErrorString(e));
       break;
@@ -599,6 +633,9 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   }
   delete P;
   delete DI;
+  if (host_prof)
+    std::fprintf(stderr, "[wino host] sweep dims=%d m=%d r=%d cands=%d launches=%d: build %.0f us, shape %.0f us, enqueue %.0f us\n",
+                 dims, m, r, n_cand, launches, t_build, t_occ, t_launch);
   count_launches(launches);
   return status;
 }
