@@ -37,14 +37,21 @@ CASES = [
     (2, 6, 5, [OP.n10_c1c2(0.39, 0.78)], 0),                               # generic shared-memory
     (2, 2, 3, [OP.f23_c(0.5), OP.f23_c(1.5)], 0),
     (2, 4, 3, [OP.f43_c(1.6), OP.f43_c(0.7)], 2),                          # Huffman order
+    (2, 4, 3, [OP.f43_c(1.6), OP.f43_c(0.7), OP.f43_c(1e19)], 2 | 256),    # Huffman, run-time kernels
+    (1, 6, 3, [OP.n8_cd(2.0, 1.003)], 2 | 256),                            # (1D)
+    (2, 8, 3, [OP.n10_c1c2(1.272, 2.099)], 2 | 256),                       # (n = 10: > 48 KB shared memory)
     (1, 6, 3, [OP.n8_cd(2.0, 1.003)], 4),                                  # mixed precision
+    (2, 8, 3, [OP.chebyshev(10)], 0),                                      # dense generic, rolled loops
 ]
+JIT = 256   # test-only marker: force the run-time specialised Huffman kernels
 
 
 @pytest.mark.parametrize("dims,m,r,sets,flags", CASES)
 def test_sweep_writes_stay_in_bounds(dims, m, r, sets, flags):
     import torch
     from paper_2201_10369_b200 import api
+    prev = api.wino_huffman_jit_mode(1 if flags & JIT else 2)
+    flags &= ~JIT
     n = m + r - 1
     T = 1237
     d, g = synth.random_tiles(T, dims, n, r, "uniform", seed=51)
@@ -58,7 +65,10 @@ def test_sweep_writes_stay_in_bounds(dims, m, r, sets, flags):
     maxs, check_m = _guarded(torch, (S, 2), torch.float64, 0.0)
     wsb = api.wino_error_sweep_workspace_bytes(dims, m, r, S, T)
     ws, check_w = _guarded(torch, (wsb,), torch.uint8, 0, guard=8192)
-    api.wino_sweep_outputs(dims, m, r, np.array(sets), dd, gg, y, ws, sums, maxs, flags=flags)
+    try:
+        api.wino_sweep_outputs(dims, m, r, np.array(sets), dd, gg, y, ws, sums, maxs, flags=flags)
+    finally:
+        api.wino_huffman_jit_mode(prev)
     for c in (check_d, check_g, check_y, check_s, check_m, check_w):
         c()
 
