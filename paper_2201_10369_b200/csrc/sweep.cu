@@ -418,7 +418,13 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
   std::vector<int> pos_status(cmax);
   std::vector<uint64_t> pos_nz((size_t)cmax * 6);
   std::vector<int> ok(std::max(n_cand, 1), 0);
-  const int build_threads = std::max(1, std::min(8, omp_get_max_threads()));
+  // host threads for the chunk builds: <= 8, and a fair share of the cores when several
+  // ranks of one node build at once (torchrun exports LOCAL_WORLD_SIZE)
+  static const int build_threads = [] {
+    int ranks = 1;
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, std::atoi(e));
+    return std::max(1, std::min({8, omp_get_max_threads(), omp_get_num_procs() / ranks}));
+  }();
   int i = 0;
   int status = WINO_OK;
   // WINO_HOST_PROFILE=1: per call, the host time spent building matrices, choosing the
