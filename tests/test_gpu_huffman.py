@@ -194,3 +194,19 @@ def test_huffman_paper_tables_on_gpu(dims):
                 assert -0.04 <= rel <= 0.20
             else:
                 assert -0.04 <= rel <= 0.09, (n, row["kind"], rel)
+
+
+def test_huffman_rejected_candidates(huffman_kernel):
+    """Rejected candidates (duplicate / NaN points) between accepted ones: statuses per
+    candidate, NaN statistics rows, the accepted rows equal to the oracle's Huffman mode --
+    on both kernels (the run-time kernels sort candidates by class; rejected ones have none)."""
+    sets = [OP.f43_c(1.7), [0.0, 1.0, 1.0, -1.0, 2.0, INF], [math.nan] * 6, OP.f43_c(0.9), OP.f43_c(1.7)]
+    d, g = synth.random_tiles(3001, 2, 6, 3, "uniform", seed=15)
+    st, s, mx = _stats(2, 4, 3, sets, d, g)
+    assert st.tolist() == [0, 3, 5, 0, 0]
+    assert np.all(np.isnan(s[1:3])) and np.all(np.isnan(mx[1:3]))
+    s_ref, m_ref, _ = ref.sweep(2, 4, 3, [sets[0], sets[3], sets[4]], d, g, huffman=True)
+    ok = [0, 3, 4]
+    assert np.array_equal(s[ok, 3:], s_ref[:, 3:]) and np.array_equal(mx[ok], m_ref)
+    assert np.all(np.abs(s[ok, 0] / s_ref[:, 0] - 1) < 1e-12)
+    assert np.array_equal(s[0], s[4])   # same point set, same class: bitwise equal rows
