@@ -17,7 +17,6 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
-#include <cstdlib>
 
 #include "tc_gemm.cuh"
 #include "wino_internal.h"
@@ -45,10 +44,6 @@ struct Geo {
   long long Tp;
   int tf32;        // 1: U / V rounded to TF32 (nearest, ties away) for the tcgen05 variant;
                    // 2: 3xTF32 -- hi = tf32(x) in plane p, lo = tf32(x - hi) in plane NN + p
-  // tile chunk processed by one K2 -> K3 -> K4 pass: tiles [t0, t0 + Tn) of the layer, held in
-  // V / M chunk buffers of Tc tile columns (Tc a multiple of 128, Tn <= Tc); an unchunked
-  // layer is one chunk with t0 = 0, Tn = T, Tc = Tp
-  long long t0, Tn, Tc;
 };
 
 // round-to-nearest fp32 -> TF32 (10 explicit mantissa bits); the tensor core would otherwise
@@ -74,9 +69,6 @@ Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, int tf32 
   g.Kp = (!tf32 && K <= 64) ? 64 : (K + 127) / 128 * 128;
   g.Tp = (g.T + ta - 1) / ta * ta;
   g.tf32 = tf32;
-  g.t0 = 0;
-  g.Tn = g.T;
-  g.Tc = g.Tp;
   return g;
 }
 
@@ -144,14 +136,13 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
   constexpr int N = M + R - 1;
   constexpr int kInCpt = in_cpt<N>();
   static_assert(N <= 16, "row / column masks are 16 bits");
-  const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp / kInCpt * Tc
-  if (gidx >= (long long)(geo.Cp / kInCpt) * geo.Tc) return;
-  const long long tl = gidx % geo.Tc;            // column in the chunk buffer
-  const long long t = geo.t0 + tl;               // tile of the layer
-  const int c0 = (int)(gidx / geo.Tc) * kInCpt;
-  const long long plane = (long long)geo.Cp * geo.Tc;
+  const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp / kInCpt * Tp
+  if (gidx >= (long long)(geo.Cp / kInCpt) * geo.Tp) return;
+  const long long t = gidx % geo.Tp;
+  const int c0 = (int)(gidx / geo.Tp) * kInCpt;
+  const long long plane = (long long)geo.Cp * geo.Tp;
   const long long lo_off = (long long)N * N * plane;   // 3xTF32 lo planes
-  const bool tile_ok = tl < geo.Tn;
+  const bool tile_ok = t < geo.T;
   int img = 0, h0 = 0, w0 = 0;
   unsigned rowm = 0, colm = 0;
   if (tile_ok) {
@@ -170,7 +161,7 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
 #pragma unroll 1
   for (int cc = 0; cc < kInCpt; cc++) {
     const int c = c0 + cc;
-    float* dst = V + (long long)c * geo.Tc + tl;
+    float* dst = V + (long long)c * geo.Tp + t;
     if (!tile_ok || c >= geo.C) {
 #pragma unroll
       for (int p = 0; p < N * N; p++) {
@@ -335,13 +326,12 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
                                                                            const __grid_constant__ LayerMats mt,
                                                                            float* __restrict__ act, int pool) {
   constexpr int N = M + R - 1;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * Tn
-  if (idx >= (long long)geo.K * geo.Tn) return;
-  const long long tl = idx % geo.Tn;             // column in the chunk buffer
-  const long long t = geo.t0 + tl;               // tile of the layer
-  const int k = (int)(idx / geo.Tn);
-  const long long plane = (long long)geo.Kp * geo.Tc;
-  const float* src = Mw + (long long)k * geo.Tc + tl;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * T
+  if (idx >= (long long)geo.K * geo.T) return;
+  const long long t = idx % geo.T;
+  const int k = (int)(idx / geo.T);
+  const long long plane = (long long)geo.Kp * geo.Tp;
+  const float* src = Mw + (long long)k * geo.Tp + t;
   // T3[p][l] = Σ_i Aᵀ[p][i] Mw[i][l]: rows of Mw streamed in ascending i (each (p, l) is
   // still one ascending fmaf chain from +0)
   float t3[M][N];
@@ -754,57 +744,15 @@ const LayerCfg* find_layer(int m, int r) {
   return nullptr;
 }
 
-// Tile chunking of the FFMA path.  V and M are produced and consumed chunk by chunk: chunk i
-// runs K2 -> K3 -> K4 in order on pipeline stream i % NS with its own V / M chunk buffers
-// (NS sets), so NS chunks are in flight at once -- the HBM / issue-bound transforms of one
-// chunk overlap the FP32-bound GEMM of another, a GEMM's partial last wave is filled by the
-// next chunk's, and a chunk's V / M can stay resident in L2 between the kernel that writes
-// them and the one that reads them (the buffers are reused, so their lines are overwritten
-// in L2).  Every element is computed by the same thread program from the same inputs as in
-// the unchunked pass, so the results are identical.  Budget: bytes of ONE V + M chunk pair
-// (WINO_LAYER_CHUNK_MB, read per call so the workspace query and the launch agree; 0 = one
-// chunk); NS from WINO_LAYER_STREAMS (1..kMaxNS).
-constexpr int kMaxNS = 4;
-double chunk_budget_bytes() {
-  double mb = 64.0;
-  if (const char* e = std::getenv("WINO_LAYER_CHUNK_MB")) mb = std::atof(e);
-  return mb * 1048576.0;
-}
-int pipeline_streams() {
-  int ns = 2;
-  if (const char* e = std::getenv("WINO_LAYER_STREAMS")) ns = std::atoi(e);
-  return std::max(1, std::min(kMaxNS, ns));
-}
-
-// Tc: tile columns per chunk buffer (a multiple of 128, chunks balanced); Tp = one chunk
-Geo plan_chunks(Geo g) {
-  const int n = g.m + g.r - 1, nn = n * n;
-  g.Tc = g.Tp;
-  if (g.tf32 || g.T == 0) return g;   // the tcgen05 variants run unchunked
-  const double per_block = (double)nn * (g.Cp + g.Kp) * 128.0 * sizeof(float);
-  const double budget = chunk_budget_bytes();
-  const long long blocks = g.Tp / 128;
-  if (budget <= 0.0) return g;
-  const long long per = std::max(1LL, (long long)(budget / per_block));
-  if (per >= blocks) return g;
-  const long long nch = (blocks + per - 1) / per;
-  g.Tc = (blocks + nch - 1) / nch * 128;
-  return g;
-}
-
 struct WsLayout {
   size_t u_off, v_off, m_off, p_off, total;
-  size_t v_stride, m_stride;   // bytes between chunk buffers
-  int nbuf;
 };
 
-// per-thread, per-device side streams + events for layer_launch: the filter transform's
-// stream and the chunk pipeline's streams, forked from and joined to the caller's stream
-// with events (graph-capture compatible)
+// per-thread, per-device side stream + fork/join events for layer_launch
 struct SideStream {
   bool ok = false;
-  cudaStream_t s = nullptr, ps[kMaxNS] = {};
-  cudaEvent_t fork = nullptr, join = nullptr, done[kMaxNS] = {};
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_stream() {
   thread_local SideStream per_dev[64];
@@ -812,10 +760,9 @@ SideStream& side_stream() {
   cudaGetDevice(&dev);
   SideStream& ss = per_dev[dev & 63];
   if (!ss.ok && ss.s == nullptr) {
-    auto ev = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
-    auto st = [](cudaStream_t* s) { return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) == cudaSuccess; };
-    ss.ok = st(&ss.s) && ev(&ss.fork) && ev(&ss.join);
-    for (int b = 0; b < kMaxNS; b++) ss.ok = ss.ok && st(&ss.ps[b]) && ev(&ss.done[b]);
+    ss.ok = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) == cudaSuccess;
   }
   return ss;
 }
@@ -825,13 +772,9 @@ WsLayout ws_layout(const Geo& g) {
   WsLayout L;
   L.u_off = 0;
   const size_t planes = g.tf32 == 2 ? 2 : 1;   // 3xTF32: hi and lo planes of U and V
-  const int nbuf = g.Tc < g.Tp ? (int)std::min<long long>(pipeline_streams(), (g.Tp + g.Tc - 1) / g.Tc) : 1;
-  L.nbuf = nbuf;
   L.v_off = L.u_off + align_up(planes * nn * g.Cp * g.Kp * sizeof(float), 256);
-  L.v_stride = nbuf > 1 ? align_up(planes * nn * g.Cp * g.Tc * sizeof(float), 256) : 0;
-  L.m_off = L.v_off + align_up(planes * nn * g.Cp * g.Tc * sizeof(float), 256) * nbuf;
-  L.m_stride = nbuf > 1 ? align_up((size_t)nn * g.Kp * g.Tc * sizeof(float), 256) : 0;
-  L.p_off = L.m_off + align_up((size_t)nn * g.Kp * g.Tc * sizeof(float), 256) * nbuf;
+  L.m_off = L.v_off + align_up(planes * nn * g.Cp * g.Tp * sizeof(float), 256);
+  L.p_off = L.m_off + align_up((size_t)nn * g.Kp * g.Tp * sizeof(float), 256);
   const dim3 sg = score_grid(g);
   L.total = L.p_off + align_up((size_t)sg.x * sg.y * sg.z * 8 * sizeof(double), 256);
   return L;
@@ -870,8 +813,8 @@ int relu_pool_launch(const float* x, float* y, int N, int C, int H, int W, int p
 int layer_supported(int m, int r) { return find_layer(m, r) != nullptr; }
 
 size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m) {
-  // large enough for the (chunked) FFMA path and the tcgen05 variants
-  return std::max(ws_layout(plan_chunks(make_geo(N, C, H, W, K, r, pad, m, 0))).total,
+  // large enough for the FFMA path and the tcgen05 variant's alignments
+  return std::max(ws_layout(make_geo(N, C, H, W, K, r, pad, m, 0)).total,
                   ws_layout(make_geo(N, C, H, W, K, r, pad, m, 2)).total);
 }
 
@@ -881,7 +824,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   const LayerCfg* cfg = find_layer(m, r);
   if (!cfg) return set_error(WINO_E_UNSUPPORTED, "no layer kernel for m=%d r=%d", m, r);
   const int tf32 = (flags & WINO_CONV_3XTF32) ? 2 : (flags & WINO_CONV_TF32) ? 1 : 0;
-  const Geo g = plan_chunks(make_geo(N, C, H, W, K, r, pad, m, tf32));
+  const Geo g = make_geo(N, C, H, W, K, r, pad, m, tf32);
   const WsLayout L = ws_layout(g);
   if (!workspace || ws_bytes < L.total)
     return set_error(WINO_E_WORKSPACE, "layer workspace %zu < %zu bytes", ws_bytes, L.total);
@@ -896,19 +839,17 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   const XformK& xk = pick_xform(*cfg, mt, m, n);
   char* ws = reinterpret_cast<char*>(workspace);
   float* U = reinterpret_cast<float*>(ws + L.u_off);
+  float* V = reinterpret_cast<float*>(ws + L.v_off);
+  float* Mw = reinterpret_cast<float*>(ws + L.m_off);
   double* partial = reinterpret_cast<double*>(ws + L.p_off);
   const int tpb = 256;
   int launches = 0;
-  const long long n_chunks = (g.Tp + g.Tc - 1) / g.Tc;
-  // K1 (filter) runs on a side stream forked from `stream` and hides under the first input
-  // transforms.  With several chunks, chunk ci runs on pipeline stream ci % nbuf (above);
-  // every side stream is joined back into `stream` before the call returns.
+  // K1 (filter) and K2 (input) are independent: K1 runs on a per-thread, per-device side
+  // stream forked from / joined to `stream` with events (graph-capture compatible), so the
+  // small filter transform hides under the input transform.
   SideStream& side = side_stream();
-  const bool forked = side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
-                      cudaStreamWaitEvent(side.s, side.fork, 0) == cudaSuccess;
-  bool piped = forked && L.nbuf > 1;
-  for (int b = 0; piped && b < L.nbuf; b++) piped = cudaStreamWaitEvent(side.ps[b], side.fork, 0) == cudaSuccess;
-  const int nps = piped ? L.nbuf : 1;
+  bool forked = side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
+                cudaStreamWaitEvent(side.s, side.fork, 0) == cudaSuccess;
   cudaStream_t fs = forked ? side.s : stream;
   {
     const long long tot = (long long)g.Cp * g.Kp;
@@ -918,27 +859,15 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     launches++;
   }
   if (forked) cudaEventRecord(side.join, fs);
-  const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
-  if (!tf32 && g.Kp == 64)
-    cudaFuncSetAttribute((const void*)gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<64>());
-  else if (!tf32)
-    cudaFuncSetAttribute((const void*)gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<128>());
-  for (long long ci = 0; ci < n_chunks; ci++) {
-    const int b = (int)(ci % nps);
-    const cudaStream_t cs = piped ? side.ps[b] : stream;
-    Geo gc = g;
-    gc.t0 = ci * g.Tc;
-    gc.Tn = std::min(g.Tc, g.T - gc.t0);
-    float* V = reinterpret_cast<float*>(ws + L.v_off + b * L.v_stride);
-    float* Mw = reinterpret_cast<float*>(ws + L.m_off + b * L.m_stride);
-    {   // K2 -> V[b]
-      const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
-      const long long tot = (long long)(g.Cp / cpt) * g.Tc;
-      const auto ik = xk.ik;
-      timed_launch("layer_input", cs, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, cs>>>(x, V, gc, mt); });
-      launches++;
-    }
-    if (ci < nps && forked) cudaStreamWaitEvent(cs, side.join, 0);   // U ready
+  {
+    const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
+    const long long tot = (long long)(g.Cp / cpt) * g.Tp;
+    const auto ik = xk.ik;
+    timed_launch("layer_input", stream, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt); });
+    launches++;
+  }
+  if (forked) cudaStreamWaitEvent(stream, side.join, 0);
+  {
     if (tf32) {
       // per call (cheap), so several devices / host threads in one process stay correct
       const auto kern = tf32 == 2 ? gemm_tf32_kernel<3> : gemm_tf32_kernel<1>;
@@ -962,39 +891,38 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
       else
         tmUl = tmU, tmVl = tmV;
       if (!enc) return set_error(WINO_E_CUDA, "cuTensorMapEncodeTiled failed for the tf32 contraction");
-      timed_launch(tf32 == 2 ? "layer_gemm_3xtf32" : "layer_gemm_tf32", cs, [&] {
-        kern<<<grid, tc::kThreads, smem, cs>>>(tmU, tmV, tmUl, tmVl, tmM, g.Cp, g.Kp, g.Tp, n * n);
-      });
-    } else if (g.Kp == 64) {
-      dim3 grid((unsigned)(g.Tc / BN), 1u, (unsigned)(n * n));
-      timed_launch("layer_gemm", cs, [&] {
-        gemm_kernel<64><<<grid, 128, gemm_smem<64>(), cs>>>(U, V, Mw, g.Cp, g.Kp, g.Tc);
+      timed_launch(tf32 == 2 ? "layer_gemm_3xtf32" : "layer_gemm_tf32", stream, [&] {
+        kern<<<grid, tc::kThreads, smem, stream>>>(tmU, tmV, tmUl, tmVl, tmM, g.Cp, g.Kp, g.Tp, n * n);
       });
     } else {
-      dim3 grid((unsigned)(g.Tc / BN), (unsigned)(g.Kp / 128), (unsigned)(n * n));
-      timed_launch("layer_gemm", cs, [&] {
-        gemm_kernel<128><<<grid, 256, gemm_smem<128>(), cs>>>(U, V, Mw, g.Cp, g.Kp, g.Tc);
-      });
+      if (g.Kp == 64) {
+        dim3 grid((unsigned)(g.Tp / BN), 1u, (unsigned)(n * n));
+        cudaFuncSetAttribute((const void*)gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<64>());
+        timed_launch("layer_gemm", stream, [&] {
+          gemm_kernel<64><<<grid, 128, gemm_smem<64>(), stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+        });
+      } else {
+        dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / 128), (unsigned)(n * n));
+        cudaFuncSetAttribute((const void*)gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<128>());
+        timed_launch("layer_gemm", stream, [&] {
+          gemm_kernel<128><<<grid, 256, gemm_smem<128>(), stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+        });
+      }
     }
     launches++;
-    // K4 (+ fused ReLU / pool epilogue; odd m with pool 2 runs the separate ReLU / pool
-    // kernel on y after the layer)
-    {
-      const long long tot = (long long)g.K * gc.Tn;
-      const auto ok = xk.ok;
-      timed_launch("layer_output", cs, [&] {
-        ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, cs>>>(Mw, y, gc, mt, fuse ? act : nullptr, pool);
-      });
-      launches++;
-    }
   }
-  if (piped) {   // join every pipeline stream
-    for (int b = 0; b < nps; b++) {
-      cudaEventRecord(side.done[b], side.ps[b]);
-      cudaStreamWaitEvent(stream, side.done[b], 0);
-    }
-  } else if (forked && n_chunks == 0) {
-    cudaStreamWaitEvent(stream, side.join, 0);
+  {
+    const long long tot = (long long)g.K * g.T;
+    const auto ok = xk.ok;
+    // fused ReLU (+ 2 x 2 pool for even m) epilogue; odd m with pool 2 runs the separate
+    // ReLU / pool kernel on y after the layer
+    const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
+    timed_launch("layer_output", stream, [&] {
+      ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt, fuse ? act : nullptr, pool);
+    });
+    launches++;
   }
   if (d_sums) {
     const dim3 sg = score_grid(g);
