@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "tc_gemm.cuh"
 #include "wino_internal.h"
@@ -275,14 +276,15 @@ __global__ void __launch_bounds__(2 * BMT, 256 / BMT) gemm_kernel(const float* _
       cp_async16(&Bs[stage][row][col], Bp + ((long long)kt * BK + row) * Tp + col);
     }
   };
-  load(0, 0);
-  cp_async_commit();
-  if (nk > 1) load(1, 1);
-  cp_async_commit();
+#pragma unroll
+  for (int st = 0; st < kStages - 1; st++) {
+    if (st < nk) load(st, st);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < nk; kt++) {
-    cp_async_wait<1>();   // stage kt has landed (only the newest group may be pending)
-    __syncthreads();      // ... for every thread; stage (kt + 2) % 3 was consumed at kt - 1
-    if (kt + 2 < nk) load((kt + 2) % kStages, kt + 2);
+    cp_async_wait<kStages - 2>();   // stage kt has landed (only the newest kStages - 2 groups may be pending)
+    __syncthreads();                // ... for every thread; stage (kt - 1) % kStages was consumed at kt - 1
+    if (kt + kStages - 1 < nk) load((kt + kStages - 1) % kStages, kt + kStages - 1);
     cp_async_commit();
     const int cur = kt % kStages;
 #pragma unroll
@@ -409,6 +411,236 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
         }
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------ K2+K3+K4 fused, C <= 4
+// First layers (VGG's / CIFAR stacks' RGB input, C = 3): the unfused pipeline pads C to 16
+// and round-trips V and M (n² K T floats: 1.5 GB each way for VGG conv1_1 x64) through HBM
+// for a 3-term contraction.  Here one thread owns a tile: it transforms its C input patches
+// into shared memory (sV [C][n²][128 tiles], conflict-free), then for every PAIR of output
+// channels (k, k+1) of the CTA's 16 forms Mw = Σ_c U ⊙ V (ascending c from +0, the
+// canonical chain) and the output transform in registers as FFMA2 with the two channels in
+// the halves of each register pair, and runs the same crop / ReLU / pool epilogue as K4.
+// U pairs of the CTA's channels are staged once ([k pair][c][n² padded to even] u64, read
+// as 16-byte broadcasts).  HBM traffic = x + U slice + outputs.  Per element the operations
+// and their order are exactly K2 / K3 / K4's (padding channels of K3 add fma(0, 0, acc) =
+// acc), so the result is bit-identical to the unfused path and the oracle.
+constexpr int kSmcC = 4;     // max input channels
+constexpr int kSmcKG = 16;   // output channels per CTA (multiple of 2; divides Kp)
+constexpr int kSmcT = 128;   // tiles = threads per CTA
+
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ void unpack2(u64 v, float& lo, float& hi) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
+// one row (P of the tile, image row h) of one output channel: y and / or the fused
+// activation; identical to K4's epilogue
+template <int M, int P>
+__device__ __forceinline__ void smc_emit_row(const float (&yr)[M], float (&prev)[M], int h, int tx, float* yk, float* ak,
+                                             int pool, bool pairs, const Geo& geo, int Hp, int Wp) {
+  const int wmax = geo.Wo - tx * M;
+  if (yk != nullptr && h < geo.Ho) {
+    float* row = yk + (long long)h * geo.Wo + tx * M;
+    if (pairs) {
+#pragma unroll
+      for (int s = 0; s + 1 < M; s += 2)
+        if (s < wmax) *reinterpret_cast<float2*>(row + s) = make_float2(yr[s], yr[s + 1]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < M; s++)
+        if (s < wmax) row[s] = yr[s];
+    }
+  }
+  if (ak != nullptr) {
+    if (pool == 1) {
+      if (h < geo.Ho) {
+        float* row = ak + (long long)h * geo.Wo + tx * M;
+        if (pairs) {   // Wo even and both base pointers 8-byte aligned (checked by the kernel)
+#pragma unroll
+          for (int s = 0; s + 1 < M; s += 2)
+            if (s < wmax) *reinterpret_cast<float2*>(row + s) = make_float2(fmaxf(yr[s], 0.0f), fmaxf(yr[s + 1], 0.0f));
+        } else {
+#pragma unroll
+          for (int s = 0; s < M; s++)
+            if (s < wmax) row[s] = fmaxf(yr[s], 0.0f);
+        }
+      }
+    } else if (M % 2 == 0) {
+      if (P % 2 == 0) {
+#pragma unroll
+        for (int s = 0; s < M; s++) prev[s] = yr[s];
+      } else if (h / 2 < Hp) {
+        float* row = ak + (long long)(h / 2) * Wp + tx * (M / 2);
+#pragma unroll
+        for (int s = 0; s + 1 < M; s += 2)
+          if (tx * (M / 2) + s / 2 < Wp)
+            row[s / 2] = fmaxf(fmaxf(fmaxf(prev[s], prev[s + 1]), fmaxf(yr[s], yr[s + 1])), 0.0f);
+      }
+    }
+  }
+}
+
+template <int M, int N, int Z, int P>
+__device__ __forceinline__ void smc_rows(const u64 (&t3)[M][N], const LayerMats& mt, float (&prev0)[M], float (&prev1)[M],
+                                         int ty, int tx, float* yk0, float* yk1, float* ak0, float* ak1, int pool,
+                                         bool pairs, const Geo& geo, int Hp, int Wp) {
+  if constexpr (P < M) {
+    float y0[M], y1[M];
+#pragma unroll
+    for (int s = 0; s < M; s++) {
+      u64 acc = 0ull;
+#pragma unroll
+      for (int l = 0; l < N; l++)
+        if (nzA<Z>(s * N + l)) acc = ffma2_bcast(t3[P][l], mt.AT[s * N + l], acc);
+      unpack2(acc, y0[s], y1[s]);
+    }
+    const int h = ty * M + P;
+    smc_emit_row<M, P>(y0, prev0, h, tx, yk0, ak0, pool, pairs, geo, Hp, Wp);
+    if (yk1 != nullptr || ak1 != nullptr) smc_emit_row<M, P>(y1, prev1, h, tx, yk1, ak1, pool, pairs, geo, Hp, Wp);
+    smc_rows<M, N, Z, P + 1>(t3, mt, prev0, prev1, ty, tx, yk0, yk1, ak0, ak1, pool, pairs, geo, Hp, Wp);
+  }
+}
+
+template <int N>
+constexpr int smc_nnp() { return (N * N + 1) / 2 * 2; }
+template <int N>
+size_t smc_smem(int C) {
+  return (size_t)C * N * N * kSmcT * sizeof(float) + (size_t)(kSmcKG / 2) * C * smc_nnp<N>() * sizeof(u64);
+}
+
+template <int M, int R, int Z>
+__global__ void __launch_bounds__(kSmcT, 2) smallc_kernel(const float* __restrict__ x, const float* __restrict__ U,
+                                                         float* __restrict__ y, Geo geo,
+                                                         const __grid_constant__ LayerMats mt, float* __restrict__ act,
+                                                         int pool) {
+  constexpr int N = M + R - 1, NN = N * N, NNP = smc_nnp<N>();
+  extern __shared__ __align__(16) float smc_sm[];
+  float* sV = smc_sm;                                                       // [C][NN][kSmcT]
+  u64* sU = reinterpret_cast<u64*>(smc_sm + (size_t)geo.C * NN * kSmcT);    // [kSmcKG/2][C][NNP]
+  const int tid = threadIdx.x;
+  const long long t = (long long)blockIdx.x * kSmcT + tid;
+  const int k0 = blockIdx.y * kSmcKG;
+  {
+    // U [NN][Cp][Kp] -> (k, k+1) pairs; k0 + 2 kp is even and Kp is a multiple of 64, so the
+    // 8-byte reads are aligned and stay inside the (zero-filled) padded rows
+    const long long uplane = (long long)geo.Cp * geo.Kp;
+    for (int idx = tid; idx < (kSmcKG / 2) * geo.C * NNP; idx += kSmcT) {
+      const int p = idx % NNP, c = (idx / NNP) % geo.C, kp = idx / (NNP * geo.C);
+      sU[idx] = p < NN ? *reinterpret_cast<const u64*>(U + (long long)p * uplane + (long long)c * geo.Kp + k0 + 2 * kp)
+                       : 0ull;
+    }
+  }
+  const bool tile_ok = t < geo.T;
+  int ty = 0, tx = 0, img = 0;
+  if (tile_ok) {
+    const int per_img = geo.th * geo.tw;
+    img = (int)(t / per_img);
+    const int rem = (int)(t - (long long)img * per_img);
+    ty = rem / geo.tw;
+    tx = rem - ty * geo.tw;
+    const int h0 = ty * M - geo.pad, w0 = tx * M - geo.pad;
+    unsigned rowm = 0, colm = 0;
+#pragma unroll
+    for (int a = 0; a < N; a++) rowm |= (h0 + a >= 0 && h0 + a < geo.H) ? 1u << a : 0u;
+#pragma unroll
+    for (int b = 0; b < N; b++) colm |= (w0 + b >= 0 && w0 + b < geo.W) ? 1u << b : 0u;
+    const long long off0 = (long long)h0 * geo.W + w0;
+#pragma unroll 1
+    for (int c = 0; c < geo.C; c++) {
+      const float* xc = x + ((long long)img * geo.C + c) * geo.H * geo.W + off0;
+      float d[N][N];
+#pragma unroll
+      for (int a = 0; a < N; a++)
+#pragma unroll
+        for (int b = 0; b < N; b++)
+          d[a][b] = ((rowm >> a) & (colm >> b) & 1u) ? __ldg(xc + (long long)a * geo.W + b) : 0.0f;
+      float t2[N][N];
+#pragma unroll
+      for (int q = 0; q < N; q++)
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int j = 0; j < N; j++)
+            if (nzB<Z>(i * N + j)) acc = __fmaf_rn(mt.BT[i * N + j], d[j][q], acc);
+          t2[i][q] = acc;
+        }
+      float* dst = sV + (size_t)c * NN * kSmcT + tid;
+#pragma unroll
+      for (int i = 0; i < N; i++)
+#pragma unroll
+        for (int l = 0; l < N; l++) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int q = 0; q < N; q++)
+            if (nzB<Z>(l * N + q)) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
+          dst[(i * N + l) * kSmcT] = acc;
+        }
+    }
+  }
+  __syncthreads();
+  if (!tile_ok) return;
+  const int Hp = geo.Ho / 2, Wp = geo.Wo / 2;
+  const bool pairs = (M % 2 == 0) && (geo.Wo % 2 == 0) && (reinterpret_cast<uintptr_t>(y) % 8 == 0) &&
+                     (reinterpret_cast<uintptr_t>(act) % 8 == 0);
+  const long long ysz = (long long)geo.Ho * geo.Wo, asz = pool == 2 ? (long long)Hp * Wp : ysz;
+  const float* sv = sV + tid;
+#pragma unroll 1
+  for (int kp = 0; kp < kSmcKG / 2; kp++) {
+    const int k = k0 + 2 * kp;
+    if (k >= geo.K) break;
+    const u64* su = sU + (size_t)kp * geo.C * NNP;
+    u64 t3[M][N];
+#pragma unroll
+    for (int p = 0; p < M; p++)
+#pragma unroll
+      for (int l = 0; l < N; l++) t3[p][l] = 0ull;
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+      u64 mw[N];
+#pragma unroll
+      for (int l = 0; l < N; l++) mw[l] = 0ull;
+#pragma unroll
+      for (int c = 0; c < kSmcC; c++) {
+        if (c < geo.C) {
+          // U pairs of positions i N .. i N + N - 1 as 16-byte broadcast loads (even position
+          // pairs; NNP is even, so every channel row starts 16-byte aligned)
+          const u64* suc = su + c * NNP;
+          const float* svc = sv + (size_t)c * NN * kSmcT;
+#pragma unroll
+          for (int j = (i * N) / 2; j <= (i * N + N - 1) / 2; j++) {
+            const ulonglong2 u2 = *reinterpret_cast<const ulonglong2*>(suc + 2 * j);
+            const int q0 = 2 * j, q1 = 2 * j + 1;
+            if (q0 >= i * N && q0 < i * N + N) {
+              const float v = svc[q0 * kSmcT];
+              mw[q0 - i * N] = ffma2_bcast(u2.x, v, mw[q0 - i * N]);
+            }
+            if (q1 >= i * N && q1 < i * N + N) {
+              const float v = svc[q1 * kSmcT];
+              mw[q1 - i * N] = ffma2_bcast(u2.y, v, mw[q1 - i * N]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < M; p++)
+        if (nzA<Z>(p * N + i))
+#pragma unroll
+          for (int l = 0; l < N; l++) t3[p][l] = ffma2_bcast(mw[l], mt.AT[p * N + i], t3[p][l]);
+    }
+    const bool k1 = k + 1 < geo.K;
+    float* yk0 = y ? y + ((long long)img * geo.K + k) * ysz : nullptr;
+    float* yk1 = (y && k1) ? yk0 + ysz : nullptr;
+    float* ak0 = act ? act + ((long long)img * geo.K + k) * asz : nullptr;
+    float* ak1 = (act && k1) ? ak0 + asz : nullptr;
+    float prev0[M], prev1[M];
+    smc_rows<M, N, Z, 0>(t3, mt, prev0, prev1, ty, tx, yk0, yk1, ak0, ak1, pool, pairs, geo, Hp, Wp);
   }
 }
 
@@ -660,6 +892,8 @@ typedef void (*FilterK)(const float*, float*, int, int, int, int, int, LayerMats
 typedef void (*InputK)(const float*, float*, Geo, LayerMats);
 typedef void (*OutputK)(const float*, float*, Geo, LayerMats, float*, int);
 typedef void (*ScoreK)(const float*, const float*, const float*, Geo, ScoreTile, double*);
+typedef void (*SmallCK)(const float*, const float*, float*, Geo, LayerMats, float*, int);
+typedef size_t (*SmallCSmem)(int);
 
 // transform kernels of one structural-zero family Z (0 = dense)
 struct XformK {
@@ -667,6 +901,8 @@ struct XformK {
   uint64_t za[2], zb[2];   // skipped entries of Aᵀ / Bᵀ (zero_masks.h)
   InputK ik;
   OutputK ok;
+  SmallCK sck;            // fused C <= kSmcC kernel (NULL: not compiled for this shape)
+  SmallCSmem sck_smem;
 };
 
 struct LayerCfg {
@@ -688,6 +924,12 @@ XformK make_xform_k() {
   }
   v.ik = input_kernel<M, R, Z>;
   v.ok = output_kernel<M, R, Z>;
+  v.sck = nullptr;
+  v.sck_smem = nullptr;
+  if constexpr (R == 3 && M + R - 1 <= 8) {   // the first layers of the 3 x 3 stacks
+    v.sck = smallc_kernel<M, R, Z>;
+    v.sck_smem = smc_smem<M + R - 1>;
+  }
   return v;
 }
 
@@ -847,8 +1089,12 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   // K1 (filter) and K2 (input) are independent: K1 runs on a per-thread, per-device side
   // stream forked from / joined to `stream` with events (graph-capture compatible), so the
   // small filter transform hides under the input transform.
+  // C <= 4 (RGB first layers): K2 + K3 + K4 fused in one kernel after K1 (smallc_kernel);
+  // WINO_LAYER_NO_SMALLC=1 forces the unfused pipeline (A/B measurements, parity tests)
+  const bool no_smallc = std::getenv("WINO_LAYER_NO_SMALLC") != nullptr;
+  const bool smallc = !tf32 && !no_smallc && C <= kSmcC && xk.sck != nullptr && xk.sck_smem(C) <= 200 * 1024;
   SideStream& side = side_stream();
-  bool forked = side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
+  bool forked = !smallc && side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
                 cudaStreamWaitEvent(side.s, side.fork, 0) == cudaSuccess;
   cudaStream_t fs = forked ? side.s : stream;
   {
@@ -859,7 +1105,17 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     launches++;
   }
   if (forked) cudaEventRecord(side.join, fs);
-  {
+  if (smallc) {
+    const size_t smem = xk.sck_smem(C);
+    const auto sck = xk.sck;
+    cudaFuncSetAttribute((const void*)sck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((unsigned)((g.T + kSmcT - 1) / kSmcT), (unsigned)((K + kSmcKG - 1) / kSmcKG));
+    const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
+    timed_launch("layer_smallc", stream,
+                 [&] { sck<<<grid, kSmcT, smem, stream>>>(x, U, y, g, mt, fuse ? act : nullptr, pool); });
+    launches++;
+  }
+  if (!smallc) {
     const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
     const long long tot = (long long)(g.Cp / cpt) * g.Tp;
     const auto ik = xk.ik;
@@ -867,7 +1123,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     launches++;
   }
   if (forked) cudaStreamWaitEvent(stream, side.join, 0);
-  {
+  if (!smallc) {
     if (tf32) {
       // per call (cheap), so several devices / host threads in one process stay correct
       const auto kern = tf32 == 2 ? gemm_tf32_kernel<3> : gemm_tf32_kernel<1>;
@@ -913,7 +1169,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     }
     launches++;
   }
-  {
+  if (!smallc) {
     const long long tot = (long long)g.K * g.T;
     const auto ok = xk.ok;
     // fused ReLU (+ 2 x 2 pool for even m) epilogue; odd m with pool 2 runs the separate

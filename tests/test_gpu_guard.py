@@ -73,10 +73,11 @@ def test_sweep_writes_stay_in_bounds(dims, m, r, sets, flags):
         c()
 
 
-def test_layer_writes_stay_in_bounds():
+@pytest.mark.parametrize("C", [13, 3])   # C = 3: the fused small-C kernel
+def test_layer_writes_stay_in_bounds(C):
     import torch
     from paper_2201_10369_b200 import api
-    N, C, H, K, m = 3, 13, 21, 19, 6
+    N, H, K, m = 3, 21, 19, 6
     pts = OP.n8_cd(2.0, 1.003)
     x, w = synth.layer_inputs(N, C, H, H, K, 3, "normal", "he", seed=52)
     xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()

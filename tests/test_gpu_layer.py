@@ -131,6 +131,10 @@ def test_layer_errors():
     (1, 5, 20, 6, 8, OP.P10, 2),                      # F(8x8,3x3) layer
 ])
 def test_fused_relu_pool_equals_separate(N, C, H, K, m, pts, pool):
+    _fused_case(N, C, H, K, m, pts, pool)
+
+
+def _fused_case(N, C, H, K, m, pts, pool):
     """wino_conv2d_relu_pool_fp32: act = maxpool(ReLU(conv)) bit for bit equal to the oracle
     layer followed by the oracle's ReLU / pool; y (when requested) equals the oracle layer;
     scored statistics per image sum to the whole-batch statistics."""
@@ -160,3 +164,40 @@ def test_fused_relu_pool_equals_separate(N, C, H, K, m, pts, pool):
         api.wino_conv2d_relu_pool_fp32(xd, wd, None, act2, 1, m, pts, ws, pool)
         torch.cuda.synchronize()
         assert np.array_equal(act2.cpu().numpy(), a_ref)
+
+
+@pytest.mark.parametrize("N,C,H,K,m,pts,pool", [
+    (3, 3, 40, 21, 6, OP.n8_cd(2.0, 1.003), 2),      # RGB, 147 tiles (2 CTAs, ragged), odd K over 2 k-groups
+    (2, 3, 35, 16, 6, OP.n8_cd(2.0, 1.003), 1),      # odd H, ReLU only
+    (1, 3, 26, 33, 6, OP.chebyshev(8), 2),           # dense (no zero family) F(6x6,3x3), 3 k-groups
+    (2, 1, 20, 5, 4, OP.f43_c(1.6), 2),              # C = 1
+    (1, 4, 18, 18, 2, OP.f23_c(1.0), 2),             # C = 4
+    (2, 2, 17, 7, 3, OP.canonical([0.0, 1.0, -1.0, 0.5]), 2),   # odd m: separate pool kernel after the fused layer
+    (1, 3, 23, 9, 5, [-2.0, -1.0, 0.0, 0.5, 1.0, 2.0, INF], 1),
+])
+def test_smallc_fused_layer(N, C, H, K, m, pts, pool):
+    """C <= 4 layers run K2 + K3 + K4 as one kernel (smallc_kernel): outputs, fused
+    activation and statistics equal the oracle's bit for bit, the kernel really is the one
+    that ran, and the unfused pipeline (WINO_LAYER_NO_SMALLC=1) gives the same bits."""
+    import os
+    import torch
+    from paper_2201_10369_b200 import api
+    api.wino_timing_reset()
+    api.wino_timing_enable(True)
+    try:
+        _fused_case(N, C, H, K, m, pts, pool)
+        assert api.wino_timing_read("layer_smallc")[1] >= 1
+        assert api.wino_timing_read("layer_gemm")[1] == 0
+    finally:
+        api.wino_timing_enable(False)
+        api.wino_timing_reset()
+    x, w = synth.layer_inputs(N, C, H, H, K, 3, "normal", "he", seed=7)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    y1, _, _ = api.conv2d(xd, wd, 1, m, pts)
+    os.environ["WINO_LAYER_NO_SMALLC"] = "1"
+    try:
+        y2, _, _ = api.conv2d(xd, wd, 1, m, pts)
+    finally:
+        del os.environ["WINO_LAYER_NO_SMALLC"]
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
