@@ -217,11 +217,11 @@ def bench_layer(torch, dev, flush, steps=10, rank=0, world=1, dist=None):
     ws = torch.empty(api.wino_conv2d_workspace_bytes(Nr, C, H, W, K, r, pad, m), dtype=torch.uint8, device=dev)
 
     def sync_ranks():
-        if world > 1:
+        if dist is not None:
             dist.barrier(device_ids=[dev.index])
 
     def max_over_ranks(vals):
-        if world == 1:
+        if dist is None:
             return vals
         t = torch.tensor(vals, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -277,7 +277,7 @@ def bench_layer(torch, dev, flush, steps=10, rank=0, world=1, dist=None):
         mv = torch.zeros(2, dtype=torch.float64, device=dev)
         api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws, sv, mv, flags=flag)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist is not None:
             dist.all_reduce(sv, op=dist.ReduceOp.SUM)
         return max_over_ranks(tv), kv, sv.cpu().numpy()
 
@@ -285,7 +285,7 @@ def bench_layer(torch, dev, flush, steps=10, rank=0, world=1, dist=None):
     tf3, kern_tf3, s_tf3 = run_variant(api.WINO_CONV_3XTF32, "layer_gemm_3xtf32")
     api.wino_timing_enable(False)
     ts, sc = max_over_ranks(ts), max_over_ranks(sc)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
         dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
     s = sums.cpu().numpy() / 2
@@ -370,7 +370,10 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # WINO_FORCE_COLLECTIVES=1: initialise NCCL and run every collective of the N > 1 path
+    # also with one rank (torchrun --nproc-per-node 1) -- a 1-GPU box exercises the NCCL code
+    dist_on = world > 1 or os.environ.get("WINO_FORCE_COLLECTIVES") == "1"
+    if dist_on:
         import datetime
         # finite timeout: a rank that dies makes the others fail instead of hanging the box
         dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
@@ -390,7 +393,7 @@ def main():
         flush_buf.zero_()
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier(device_ids=[local])
 
     # ---- warm-up
@@ -415,7 +418,7 @@ def main():
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in step_ms]
     tot_ms = sum(step_ms)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
@@ -528,7 +531,7 @@ def main():
         e2e_copy_ms.append(a.elapsed_time(c))
     torch.cuda.synchronize()
     e2e_tot = sum(e2e_ms)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_tot = float(t.item())
@@ -546,7 +549,7 @@ def main():
     layer = None
     if not args.no_layer:
         layer, f_alg, b_alg, t_layer = bench_layer(torch, dev, flush, rank=rank, world=world,
-                                                   dist=dist if world > 1 else None)
+                                                   dist=dist if dist_on else None)
         t_roof = max(f_alg / (fp32_peak * 1e12), b_alg / (float(peaks.get("hbm_gbs", 6458.7)) * 1e9)) / world
         layer["roofline_frac"] = t_roof / (t_layer * 1e-3)
         layer["roofline_bound"] = "fp32 FFMA (t_roof = max(F_alg/P_fp32, B_alg/BW_hbm))"
@@ -615,7 +618,7 @@ def main():
         cpu = {"value": evals_c / dt_c, "unit": "tile-evals/s", "cores": thr, "kind": "oracle", "sample": desc,
                "seconds": dt_c}
 
-    if world > 1:
+    if dist_on:
         dist.barrier(device_ids=[local])
     if rank == 0:
         line = {
@@ -641,7 +644,7 @@ def main():
             "variants": variants,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 

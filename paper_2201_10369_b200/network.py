@@ -14,6 +14,7 @@ image's statistics depend only on that image, so the result is bitwise independe
 world size.  No activation exchange (the layers are data parallel)."""
 from __future__ import annotations
 
+import os
 from typing import Callable, List, Optional, Sequence
 
 import numpy as np
@@ -120,8 +121,9 @@ def stack_forward(layers, x, weights: Sequence, points, m: int = 6, score: bool 
         a = a2
     if not score:
         return a, None, None, outs, None
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    # (WINO_FORCE_COLLECTIVES=1: also with one rank, so a 1-GPU box exercises the NCCL call)
+    if world > 1 or (os.environ.get("WINO_FORCE_COLLECTIVES") == "1" and dist.is_initialized()):
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)   # exact: one owner per row
     per_img = np.concatenate([sums_img.cpu().numpy(), maxs_img.cpu().numpy()], axis=2)
     sums, maxs = reduce_images(per_img)

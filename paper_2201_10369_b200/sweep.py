@@ -11,7 +11,9 @@ injected for CPU (gloo) tests of the sharding / reduction logic.
 """
 from __future__ import annotations
 
+
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence
 
@@ -154,7 +156,9 @@ def run_step(rank_sweeps: Sequence[RankSweep], compute: Callable = abi_compute, 
     for rs in rank_sweeps:
         compute(rs)
         launches += rs.launches
-    if reduce and dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    # (WINO_FORCE_COLLECTIVES=1: also with one rank, so a 1-GPU box exercises the NCCL call)
+    if reduce and dist.is_available() and dist.is_initialized() and (
+            dist.get_world_size() > 1 or os.environ.get("WINO_FORCE_COLLECTIVES") == "1"):
         for f in flats:
             dist.all_reduce(f, op=dist.ReduceOp.SUM, group=group)
     return launches
