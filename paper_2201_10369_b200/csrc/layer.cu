@@ -45,6 +45,7 @@ struct Geo {
   long long Tp;
   int tf32;        // 1: U / V rounded to TF32 (nearest, ties away) for the tcgen05 variant;
                    // 2: 3xTF32 -- hi = tf32(x) in plane p, lo = tf32(x - hi) in plane NN + p
+  int bn;          // t-width of the FFMA GEMM's CTA tile (128, or 64: see make_geo)
 };
 
 // round-to-nearest fp32 -> TF32 (10 explicit mantissa bits); the tensor core would otherwise
@@ -63,11 +64,25 @@ Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, int tf32 
   g.th = (g.Ho + m - 1) / m;
   g.tw = (g.Wo + m - 1) / m;
   g.T = (long long)N * g.th * g.tw;
-  // FFMA GEMM: BK = 16, BN = 128; tcgen05 variant: BK = 32, N = 256
-  const int ca = tf32 ? 32 : 16, ta = tf32 ? 256 : 128;
+  // FFMA GEMM: BK = 16, BN = 128 or 64; tcgen05 variant: BK = 32, N = 256
+  const int ca = tf32 ? 32 : 16;
   g.Cp = (C + ca - 1) / ca * ca;
   // FFMA GEMM: 64-row tiles when K <= 64 (VGG's 64-channel layers), else 128; tcgen05: 128
   g.Kp = (!tf32 && K <= 64) ? 64 : (K + 127) / 128 * 128;
+  // FFMA GEMM CTA tile: 128 (k) x 128 (t) at 2 CTAs per SM, or 128 x 64 at 4 per SM (the
+  // same 8 x 8 register tile per thread, the same work per SM and wave): the narrow tile
+  // pads T to 64 instead of 128 and quantises the grid in half-size steps, so it is chosen
+  // when it needs fewer waves (VGG's 14 x 14 layers: T = 576 -> 5 waves of 128-wide tiles,
+  // 4 of 64-wide ones).  Fixed SM count (B200: 148) so the workspace query and the launch
+  // agree on Tp.
+  g.bn = 128;
+  if (!tf32 && g.Kp >= 128) {
+    const long long per = (long long)(g.Kp / 128) * (m + r - 1) * (m + r - 1);
+    const long long w128 = ((g.T + 127) / 128 * per + 2 * 148 - 1) / (2 * 148);
+    const long long w64 = ((g.T + 63) / 64 * per + 4 * 148 - 1) / (4 * 148);
+    if (w64 < w128) g.bn = 64;
+  }
+  const int ta = tf32 ? 256 : g.bn;
   g.Tp = (g.T + ta - 1) / ta * ta;
   g.tf32 = tf32;
   return g;
@@ -212,11 +227,12 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
 }
 
 // ------------------------------------------------------------------ K3
-// Batched SGEMM  M_p[k][t] = Σ_c U_p[c][k] V_p[c][t], BMT x 128 CTA tile (BMT = 128, or 64
-// when K <= 64 so the GEMM neither computes nor writes padded k rows), BK = 16,
-// 2 * BMT threads x (8 x 8) register tile, accumulators as FFMA2 pairs along t.
+// Batched SGEMM  M_p[k][t] = Σ_c U_p[c][k] V_p[c][t], BMT x BNT CTA tile (128 x 128;
+// 64 x 128 when K <= 64 so the GEMM neither computes nor writes padded k rows; 128 x 64
+// when that needs fewer waves, make_geo), BK = 16, BMT * BNT / 64 threads x (8 x 8) register
+// tile, accumulators as FFMA2 pairs along t.
 // cp.async 3-stage shared-memory ring; every accumulator is one ascending-c fmaf chain.
-constexpr int BN = 128, BK = 16;
+constexpr int BK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -234,21 +250,22 @@ __device__ __forceinline__ u64 ffma2_bcast(u64 a, float c, u64 acc) {
 }
 
 constexpr int kStages = 3;
-template <int BMT>
-constexpr size_t gemm_smem() { return (size_t)kStages * BK * (BMT + BN) * sizeof(float); }
+template <int BMT, int BNT>
+constexpr size_t gemm_smem() { return (size_t)kStages * BK * (BMT + BNT) * sizeof(float); }
 
-template <int BMT>
-__global__ void __launch_bounds__(2 * BMT, 256 / BMT) gemm_kernel(const float* __restrict__ U,
+template <int BMT, int BNT>
+__global__ void __launch_bounds__(BMT * BNT / 64, 32768 / (BMT * BNT)) gemm_kernel(const float* __restrict__ U,
                                                                  const float* __restrict__ V, float* __restrict__ Mo,
                                                                  int Cp, int Kp, long long Tp) {
-  constexpr int NT = 2 * BMT;                 // threads
+  constexpr int BN = BNT;
+  constexpr int NT = BMT * BNT / 64;          // threads
   constexpr int AV = BK * BMT / 4 / NT;       // float4 per thread per stage (A)
   constexpr int BV = BK * BN / 4 / NT;        // (B)
   extern __shared__ __align__(16) float gsm[];
   float (*As)[BK][BMT] = reinterpret_cast<float (*)[BK][BMT]>(gsm);
   float (*Bs)[BK][BN] = reinterpret_cast<float (*)[BK][BN]>(gsm + kStages * BK * BMT);
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;     // ty < BMT / 8
+  const int tx = tid % (BN / 8), ty = tid / (BN / 8);     // tx < BN / 8, ty < BMT / 8
   const long long t0 = (long long)blockIdx.x * BN;
   const int k0 = blockIdx.y * BMT;
   const int p = blockIdx.z;
@@ -292,7 +309,7 @@ __global__ void __launch_bounds__(2 * BMT, 256 / BMT) gemm_kernel(const float* _
       const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][BMT / 2 + ty * 4]);
       const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][tx * 4]);
-      const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][64 + tx * 4]);
+      const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][BN / 2 + tx * 4]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const u64 bv[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
@@ -307,7 +324,7 @@ __global__ void __launch_bounds__(2 * BMT, 256 / BMT) gemm_kernel(const float* _
     const int k = k0 + (i < 4 ? ty * 4 + i : BMT / 2 + ty * 4 + (i - 4));
     float* row = Mp + (long long)k * Tp + t0;
     *reinterpret_cast<ulonglong2*>(row + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
-    *reinterpret_cast<ulonglong2*>(row + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
+    *reinterpret_cast<ulonglong2*>(row + BN / 2 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
   }
 }
 
@@ -1151,21 +1168,18 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
         kern<<<grid, tc::kThreads, smem, stream>>>(tmU, tmV, tmUl, tmVl, tmM, g.Cp, g.Kp, g.Tp, n * n);
       });
     } else {
-      if (g.Kp == 64) {
-        dim3 grid((unsigned)(g.Tp / BN), 1u, (unsigned)(n * n));
-        cudaFuncSetAttribute((const void*)gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)gemm_smem<64>());
-        timed_launch("layer_gemm", stream, [&] {
-          gemm_kernel<64><<<grid, 128, gemm_smem<64>(), stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
-        });
-      } else {
-        dim3 grid((unsigned)(g.Tp / BN), (unsigned)(g.Kp / 128), (unsigned)(n * n));
-        cudaFuncSetAttribute((const void*)gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)gemm_smem<128>());
-        timed_launch("layer_gemm", stream, [&] {
-          gemm_kernel<128><<<grid, 256, gemm_smem<128>(), stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
-        });
-      }
+      auto run_gemm = [&](auto kern, int threads, size_t smem, unsigned kblocks, int bn) {
+        dim3 grid((unsigned)(g.Tp / bn), kblocks, (unsigned)(n * n));
+        cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        timed_launch("layer_gemm", stream,
+                     [&] { kern<<<grid, threads, smem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
+      };
+      if (g.Kp == 64)
+        run_gemm(gemm_kernel<64, 128>, 128, gemm_smem<64, 128>(), 1u, 128);
+      else if (g.bn == 64)
+        run_gemm(gemm_kernel<128, 64>, 128, gemm_smem<128, 64>(), (unsigned)(g.Kp / 128), 64);
+      else
+        run_gemm(gemm_kernel<128, 128>, 256, gemm_smem<128, 128>(), (unsigned)(g.Kp / 128), 128);
     }
     launches++;
   }

@@ -170,7 +170,9 @@ def _fused_case(N, C, H, K, m, pts, pool):
     (3, 3, 40, 21, 6, OP.n8_cd(2.0, 1.003), 2),      # RGB, 147 tiles (2 CTAs, ragged), odd K over 2 k-groups
     (2, 3, 35, 16, 6, OP.n8_cd(2.0, 1.003), 1),      # odd H, ReLU only
     (1, 3, 26, 33, 6, OP.chebyshev(8), 2),           # dense (no zero family) F(6x6,3x3), 3 k-groups
+    (2, 3, 19, 5, 6, OP.n8_cd(2.0, 1.003), 2),       # odd H with the fused pool (floor), ragged tiles
     (2, 1, 20, 5, 4, OP.f43_c(1.6), 2),              # C = 1
+    (1, 3, 21, 6, 4, OP.f43_c(0.7), 2),              # m = 4, odd H, fused pool
     (1, 4, 18, 18, 2, OP.f23_c(1.0), 2),             # C = 4
     (2, 2, 17, 7, 3, OP.canonical([0.0, 1.0, -1.0, 0.5]), 2),   # odd m: separate pool kernel after the fused layer
     (1, 3, 23, 9, 5, [-2.0, -1.0, 0.0, 0.5, 1.0, 2.0, INF], 1),
