@@ -28,6 +28,13 @@ full huffjit 'wino_huffjit' huff 20 1
 full n10 'sweep2d_kernel' cfg4 5 1
 full layer 'gemm_kernel|input_kernel|output_kernel' layer 3 3
 full score 'score_kernel' score 0 1
+python tools/vgg_layers.py --only 0 > $O/plain_smallc.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:smallc_kernel -s 3 -c 1 \
+    -o $O/prof_smallc python tools/vgg_layers.py --only 0 > $O/ncu_smallc.log 2>&1; echo "ncu smallc rc=$?"
+timeout 600 python tools/vgg_layers.py > $O/vgg_layers.json 2> $O/vgg_layers.err; echo "vgg layers rc=$?"
+WINO_FORCE_COLLECTIVES=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
+    --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline \
+    > $O/bench_nccl_one_rank.json 2> $O/bench_nccl_one_rank.err; echo "nccl one-rank bench rc=$?"
 timeout 900 python tools/cfg4_grid.py > $O/cfg4_grid.json 2> $O/cfg4_grid.err; echo "cfg4 rc=$?"
 timeout 900 python tools/vgg16.py > $O/vgg16.json 2> $O/vgg16.err; echo "vgg rc=$?"
 timeout 900 python tools/huffman_time.py > $O/variants_time.json 2> $O/variants_time.err; echo "variants rc=$?"
