@@ -233,20 +233,26 @@ def bench_layer(torch, dev, flush, steps=10, rank=0, world=1, dist=None):
         api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
     torch.cuda.synchronize()
     fams = ["layer_filter", "layer_input", "layer_gemm", "layer_output"]
-    api.wino_timing_reset()
-    api.wino_timing_enable(True)
+    # the layer time is measured with the library's per-launch event hook OFF (its events
+    # serialise the layer's programmatic-dependent-launch chain); the per-kernel breakdown
+    # comes from a second pass with the hook on
     ts = []
-    for _ in range(steps):
-        flush()
-        sync_ranks()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
-        b.record(stream)
-        b.synchronize()
-        ts.append(a.elapsed_time(b))
+    for hook in (False, True):
+        api.wino_timing_reset()
+        api.wino_timing_enable(hook)
+        for _ in range(steps):
+            flush()
+            sync_ranks()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            api.wino_conv2d_fp32(xd, wd, y, pad, m, pts, ws)
+            b.record(stream)
+            b.synchronize()
+            if not hook:
+                ts.append(a.elapsed_time(b))
     kern = {f: api.wino_timing_read(f)[0] / steps for f in fams}
     api.wino_timing_reset()
+    api.wino_timing_enable(False)
     # scored (fp64 direct scoring on every output)
     sc = []
     for _ in range(2):
@@ -258,6 +264,7 @@ def bench_layer(torch, dev, flush, steps=10, rank=0, world=1, dist=None):
         b.record(stream)
         b.synchronize()
         sc.append(a.elapsed_time(b))
+    api.wino_timing_enable(True)
     # NEXT row N3: the tcgen05 kind::tf32 contraction variants (not the parity path)
     def run_variant(flag, gemm_family):
         tv = []

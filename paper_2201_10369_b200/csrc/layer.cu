@@ -56,6 +56,32 @@ __device__ __forceinline__ float round_tf32(float v) {
   return __uint_as_float(r);
 }
 
+// Programmatic dependent launch (the unfused fp32 layer is the chain K1 -> K2 -> K3 -> K4 on
+// one stream): a kernel launched with the attribute may become resident while its
+// predecessor drains (after every CTA of the predecessor executed launch_dependents) and
+// must execute `wait` before it touches the predecessor's output.  K2 does not depend on K1,
+// so it runs beside it and waits only at its END -- its completion then implies K1's, which
+// is what K3's wait (on K2) relies on for U.  Without the launch attribute both instructions
+// are no-ops.
+__device__ __forceinline__ void lpdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void lpdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, bool pdl,
+                     Args&&... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = stream;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = la;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kern, KArgs(args)...);
+}
+
 Geo make_geo(int N, int C, int H, int W, int K, int r, int pad, int m, int tf32 = 0) {
   Geo g;
   g.N = N; g.C = C; g.H = H; g.W = W; g.K = K; g.r = r; g.pad = pad; g.m = m;
@@ -94,6 +120,7 @@ template <int M, int R>
 __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U, int C, int K, int Cp, int Kp, int tf32,
                               const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
+  lpdl_launch_dependents();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp * Kp, k fastest
   if (idx >= (long long)Cp * Kp) return;
   const int k = (int)(idx % Kp), c = (int)(idx / Kp);
@@ -152,8 +179,12 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
   constexpr int N = M + R - 1;
   constexpr int kInCpt = in_cpt<N>();
   static_assert(N <= 16, "row / column masks are 16 bits");
+  lpdl_launch_dependents();
   const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over Cp / kInCpt * Tp
-  if (gidx >= (long long)(geo.Cp / kInCpt) * geo.Tp) return;
+  if (gidx >= (long long)(geo.Cp / kInCpt) * geo.Tp) {
+    lpdl_wait();
+    return;
+  }
   const long long t = gidx % geo.Tp;
   const int c0 = (int)(gidx / geo.Tp) * kInCpt;
   const long long plane = (long long)geo.Cp * geo.Tp;
@@ -224,6 +255,7 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
         dst += plane;
       }
   }
+  lpdl_wait();   // K2 completes after K1 (see lpdl_wait above)
 }
 
 // ------------------------------------------------------------------ K3
@@ -265,6 +297,8 @@ __global__ void __launch_bounds__(BMT * BNT / 64, 32768 / (BMT * BNT)) gemm_kern
   float (*As)[BK][BMT] = reinterpret_cast<float (*)[BK][BMT]>(gsm);
   float (*Bs)[BK][BN] = reinterpret_cast<float (*)[BK][BN]>(gsm + kStages * BK * BMT);
   const int tid = threadIdx.x;
+  lpdl_launch_dependents();
+  lpdl_wait();   // U (K1, via K2's completion) and V (K2) are complete and visible
   const int tx = tid % (BN / 8), ty = tid / (BN / 8);     // tx < BN / 8, ty < BMT / 8
   const long long t0 = (long long)blockIdx.x * BN;
   const int k0 = blockIdx.y * BMT;
@@ -345,6 +379,7 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
                                                                            const __grid_constant__ LayerMats mt,
                                                                            float* __restrict__ act, int pool) {
   constexpr int N = M + R - 1;
+  lpdl_wait();   // M (K3) is complete and visible
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * T
   if (idx >= (long long)geo.K * geo.T) return;
   const long long t = idx % geo.T;
@@ -1110,8 +1145,14 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   // WINO_LAYER_NO_SMALLC=1 forces the unfused pipeline (A/B measurements, parity tests)
   const bool no_smallc = std::getenv("WINO_LAYER_NO_SMALLC") != nullptr;
   const bool smallc = !tf32 && !no_smallc && C <= kSmcC && xk.sck != nullptr && xk.sck_smem(C) <= 200 * 1024;
+  // Unfused fp32 path: K1 -> K2 -> K3 -> K4 as a programmatic-dependent-launch chain on
+  // `stream` (lpdl_wait above; K2 runs beside K1 without a side stream, K3 / K4 become
+  // resident while their predecessor drains).  The timing hook records events between the
+  // launches, which would serialise them, so with the hook on (and for the TF32 variants,
+  // whose GEMM has no wait) the kernels are launched plainly with K1 on the side stream.
+  const bool pdl = !tf32 && !smallc && !timing_enabled() && std::getenv("WINO_LAYER_NO_PDL") == nullptr;
   SideStream& side = side_stream();
-  bool forked = !smallc && side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
+  bool forked = !smallc && !pdl && side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
                 cudaStreamWaitEvent(side.s, side.fork, 0) == cudaSuccess;
   cudaStream_t fs = forked ? side.s : stream;
   {
@@ -1136,7 +1177,13 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
     const long long tot = (long long)(g.Cp / cpt) * g.Tp;
     const auto ik = xk.ik;
-    timed_launch("layer_input", stream, [&] { ik<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(x, V, g, mt); });
+    const dim3 igrid((unsigned)((tot + tpb - 1) / tpb));
+    timed_launch("layer_input", stream, [&] {
+      if (pdl)
+        launch_k(ik, igrid, dim3(tpb), 0, stream, true, x, V, g, mt);
+      else
+        ik<<<igrid, tpb, 0, stream>>>(x, V, g, mt);
+    });
     launches++;
   }
   if (forked) cudaStreamWaitEvent(stream, side.join, 0);
@@ -1171,8 +1218,12 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
       auto run_gemm = [&](auto kern, int threads, size_t smem, unsigned kblocks, int bn) {
         dim3 grid((unsigned)(g.Tp / bn), kblocks, (unsigned)(n * n));
         cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        timed_launch("layer_gemm", stream,
-                     [&] { kern<<<grid, threads, smem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp); });
+        timed_launch("layer_gemm", stream, [&] {
+          if (pdl)
+            launch_k(kern, grid, dim3(threads), smem, stream, true, U, V, Mw, g.Cp, g.Kp, g.Tp);
+          else
+            kern<<<grid, threads, smem, stream>>>(U, V, Mw, g.Cp, g.Kp, g.Tp);
+        });
       };
       if (g.Kp == 64)
         run_gemm(gemm_kernel<64, 128>, 128, gemm_smem<64, 128>(), 1u, 128);
@@ -1189,8 +1240,12 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
     // fused ReLU (+ 2 x 2 pool for even m) epilogue; odd m with pool 2 runs the separate
     // ReLU / pool kernel on y after the layer
     const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
+    const dim3 ogrid((unsigned)((tot + tpb - 1) / tpb));
     timed_launch("layer_output", stream, [&] {
-      ok<<<(unsigned)((tot + tpb - 1) / tpb), tpb, 0, stream>>>(Mw, y, g, mt, fuse ? act : nullptr, pool);
+      if (pdl)
+        launch_k(ok, ogrid, dim3(tpb), 0, stream, true, Mw, y, g, mt, fuse ? act : nullptr, pool);
+      else
+        ok<<<ogrid, tpb, 0, stream>>>(Mw, y, g, mt, fuse ? act : nullptr, pool);
     });
     launches++;
   }

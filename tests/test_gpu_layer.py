@@ -203,3 +203,36 @@ def test_smallc_fused_layer(N, C, H, K, m, pts, pool):
         del os.environ["WINO_LAYER_NO_SMALLC"]
     torch.cuda.synchronize()
     assert torch.equal(y1, y2)
+
+
+def test_pdl_chain_equals_plain_launches():
+    """The unfused layer runs K1 -> K2 -> K3 -> K4 as a programmatic-dependent-launch chain
+    (kernels become resident while their predecessor drains and wait before touching its
+    output).  At the configs[2] size, with the workspace dirtied between runs, every run of
+    the chain gives the same bits as plainly serialised launches (WINO_LAYER_NO_PDL=1)."""
+    import os
+    import torch
+    from paper_2201_10369_b200 import api
+    N, C, H, K, m = 32, 256, 56, 256, 6
+    pts = OP.n8_cd(2.0, 1.003)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    x = torch.randn((N, C, H, H), device="cuda", generator=g)
+    w = torch.randn((K, C, 3, 3), device="cuda", generator=g) * (2.0 / (C * 9)) ** 0.5
+    ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, H, K, 3, 1, m), dtype=torch.uint8, device="cuda")
+    y0 = torch.empty((N, K, H, H), device="cuda")
+    os.environ["WINO_LAYER_NO_PDL"] = "1"
+    try:
+        api.wino_conv2d_fp32(x, w, y0, 1, m, pts, ws)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["WINO_LAYER_NO_PDL"]
+    y = torch.empty_like(y0)
+    for it in range(6):
+        ws.fill_(0xFF)          # NaN patterns: a read before the producer finished would show
+        y.fill_(float("nan"))
+        api.wino_conv2d_fp32(x, w, y, 1, m, pts, ws)
+        if it % 2:              # back-to-back calls: the next chain starts behind this one
+            api.wino_conv2d_fp32(x, w, y, 1, m, pts, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0)

@@ -21,6 +21,12 @@ full() {   # name, kernel regex, prof_driver mode, launch-skip, launch-count
   python tools/prof_driver.py $3 > $O/plain_$1.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"$2" -s $4 -c $5 \
       -o $O/prof_$1 python tools/prof_driver.py $3 > $O/ncu_$1.log 2>&1; echo "ncu $1 rc=$?"
+  summarise $1
+}
+summarise() {   # the reports exceed gpurun's 64 MiB return limit: keep their text summaries
+  python tools/ncu_summary.py $O/prof_$1.ncu-rep --stalls > $O/ncu_$1.txt 2>&1
+  { echo; echo "# hot instructions (tools/ncu_hot.py)"; python tools/ncu_hot.py $O/prof_$1.ncu-rep 15; } >> $O/ncu_$1.txt 2>&1
+  rm -f $O/prof_$1.ncu-rep
 }
 full sweep2d 'sweep2d_reg_kernel' sweep 50 1
 full sweep1d 'sweep1d_kernel' sweep 50 1
@@ -31,6 +37,7 @@ full score 'score_kernel' score 0 1
 python tools/vgg_layers.py --only 0 > $O/plain_smallc.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:smallc_kernel -s 3 -c 1 \
     -o $O/prof_smallc python tools/vgg_layers.py --only 0 > $O/ncu_smallc.log 2>&1; echo "ncu smallc rc=$?"
+summarise smallc
 timeout 600 python tools/vgg_layers.py > $O/vgg_layers.json 2> $O/vgg_layers.err; echo "vgg layers rc=$?"
 WINO_FORCE_COLLECTIVES=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
     --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline \

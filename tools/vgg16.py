@@ -37,20 +37,22 @@ def main():
     for C, K, _, pool in network.VGG16:
         direct_flop += 2.0 * args.batch * K * C * h * h * 9
         h = h // 2 if pool else h
+    # forward time with the library's event hook off (its events would serialise the layers'
+    # programmatic-dependent-launch chains); per-kernel totals from 3 more passes with it on
     times = []
     api.wino_timing_reset()
-    for it in range(7):
-        if it == 2:
+    for it in range(10):
+        if it == 7:
             api.wino_timing_enable(True)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         network.vgg16_forward(xd, wd, pts, m=6, score=False)
         b.record()
         b.synchronize()
-        if it >= 2:
+        if 2 <= it < 7:
             times.append(a.elapsed_time(b))
-    kern = {f: api.wino_timing_read(f)[0] / len(times)
-            for f in ("layer_filter", "layer_input", "layer_gemm", "layer_output", "relu_pool")}
+    kern = {f: api.wino_timing_read(f)[0] / 3
+            for f in ("layer_filter", "layer_input", "layer_gemm", "layer_output", "layer_smallc", "relu_pool")}
     api.wino_timing_enable(False)
     t = statistics.median(times)
     xs = xd[: args.scored_batch].contiguous()
