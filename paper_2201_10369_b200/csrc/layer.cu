@@ -482,11 +482,6 @@ constexpr int kSmcC = 4;     // max input channels
 constexpr int kSmcKG = 16;   // output channels per CTA (multiple of 2; divides Kp)
 constexpr int kSmcT = 128;   // tiles = threads per CTA
 
-__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
-  u64 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
 __device__ __forceinline__ void unpack2(u64 v, float& lo, float& hi) {
   asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
