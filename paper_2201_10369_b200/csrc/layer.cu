@@ -373,12 +373,17 @@ using tc::gemm_tf32_kernel;
 // needs an even tile size so no window straddles two tiles -- the launcher only fuses then);
 // y itself is written only when y != NULL (the scorer and the caller's `keep` need it).
 // ReLU and max are exact, so the fused output equals relu_pool(y) bit for bit.
-template <int M, int R, int Z>
+// EP: the epilogue compiled in -- 0: y only; 1: ReLU activation (y optional); 2: ReLU +
+// 2 x 2 max pool (y optional).  One kernel with run-time epilogue branches cost the y-only
+// and pooled paths registers / issue slots (measured when the 8-byte ReLU stores were added).
+template <int M, int R, int Z, int EP>
 __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(const float* __restrict__ Mw,
                                                                            float* __restrict__ y, Geo geo,
                                                                            const __grid_constant__ LayerMats mt,
-                                                                           float* __restrict__ act, int pool) {
+                                                                           float* __restrict__ act_in, int) {
   constexpr int N = M + R - 1;
+  constexpr int pool = EP == 2 ? 2 : 1;
+  float* const act = EP == 0 ? nullptr : act_in;
   lpdl_wait();   // M (K3) is complete and visible
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over K * T
   if (idx >= (long long)geo.K * geo.T) return;
@@ -415,7 +420,8 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
   // rows of the output tile; even M with an even row length -> 8-byte pair stores (the
   // lanes of a warp cover consecutive tiles, so a pair store fills 1/3 of a 768 B span
   // instead of 1/6)
-  const bool pairs = (M % 2 == 0) && (geo.Wo % 2 == 0) && (reinterpret_cast<uintptr_t>(y) % 8 == 0);
+  const bool pairs = (M % 2 == 0) && (geo.Wo % 2 == 0) && (reinterpret_cast<uintptr_t>(y) % 8 == 0) &&
+                     (reinterpret_cast<uintptr_t>(act) % 8 == 0);
   float prev[M];
 #pragma unroll
   for (int p = 0; p < M; p++) {
@@ -442,13 +448,20 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 2) output_kernel(con
           if (s < wmax) row[s] = yr[s];
       }
     }
-    if (ak != nullptr) {
-      if (pool == 1) {
+    if (EP != 0 && ak != nullptr) {
+      if (EP == 1) {
         if (h < geo.Ho) {
           float* row = ak + (long long)h * geo.Wo + tx * M;
+          if (pairs) {
 #pragma unroll
-          for (int s = 0; s < M; s++)
-            if (s < wmax) row[s] = fmaxf(yr[s], 0.0f);
+            for (int s = 0; s + 1 < M; s += 2)
+              if (s < wmax)
+                *reinterpret_cast<float2*>(row + s) = make_float2(fmaxf(yr[s], 0.0f), fmaxf(yr[s + 1], 0.0f));
+          } else {
+#pragma unroll
+            for (int s = 0; s < M; s++)
+              if (s < wmax) row[s] = fmaxf(yr[s], 0.0f);
+          }
         }
       } else if (M % 2 == 0) {
         if (p % 2 == 0) {
@@ -947,7 +960,7 @@ struct XformK {
   int z;
   uint64_t za[2], zb[2];   // skipped entries of Aᵀ / Bᵀ (zero_masks.h)
   InputK ik;
-  OutputK ok;
+  OutputK ok[3];          // by epilogue: y only / ReLU / ReLU + pool
   SmallCK sck;            // fused C <= kSmcC kernel (NULL: not compiled for this shape)
   SmallCSmem sck_smem;
 };
@@ -970,7 +983,9 @@ XformK make_xform_k() {
     v.zb[w] = ZM<Z>::B(w);
   }
   v.ik = input_kernel<M, R, Z>;
-  v.ok = output_kernel<M, R, Z>;
+  v.ok[0] = output_kernel<M, R, Z, 0>;
+  v.ok[1] = output_kernel<M, R, Z, 1>;
+  v.ok[2] = output_kernel<M, R, Z, 2>;
   v.sck = nullptr;
   v.sck_smem = nullptr;
   if constexpr (R == 3 && M + R - 1 <= 8) {   // the first layers of the 3 x 3 stacks
@@ -1231,10 +1246,10 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   }
   if (!smallc) {
     const long long tot = (long long)g.K * g.T;
-    const auto ok = xk.ok;
     // fused ReLU (+ 2 x 2 pool for even m) epilogue; odd m with pool 2 runs the separate
     // ReLU / pool kernel on y after the layer
     const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
+    const auto ok = xk.ok[fuse ? (pool == 2 ? 2 : 1) : 0];
     const dim3 ogrid((unsigned)((tot + tpb - 1) / tpb));
     timed_launch("layer_output", stream, [&] {
       if (pdl)
