@@ -173,7 +173,8 @@ __global__ void filter_kernel(const float* __restrict__ w, float* __restrict__ U
 // dominates), 1 otherwise (more threads in flight); always divides Cp (a multiple of 16)
 template <int N>
 constexpr int in_cpt() { return N > 8 ? 4 : 1; }
-template <int M, int R, int Z>
+// TF: the rounding of V compiled in (Geo::tf32: 0 fp32, 1 TF32, 2 3xTF32 hi / lo planes)
+template <int M, int R, int Z, int TF>
 __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(const float* __restrict__ x, float* __restrict__ V, Geo geo,
                                                        const __grid_constant__ LayerMats mt) {
   constexpr int N = M + R - 1;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
 #pragma unroll
       for (int p = 0; p < N * N; p++) {
         dst[(long long)p * plane] = 0.0f;
-        if (geo.tf32 == 2) dst[lo_off + (long long)p * plane] = 0.0f;
+        if (TF == 2) dst[lo_off + (long long)p * plane] = 0.0f;
       }
       continue;
     }
@@ -245,12 +246,12 @@ __global__ void __launch_bounds__(256, M + R - 1 <= 8 ? 3 : 1) input_kernel(cons
 #pragma unroll
         for (int q = 0; q < N; q++)
           if (nzB<Z>(l * N + q)) acc = __fmaf_rn(t2[i][q], mt.BT[l * N + q], acc);
-        if (geo.tf32 == 2) {
+        if (TF == 2) {
           const float hi = round_tf32(acc);
           dst[0] = hi;
           dst[lo_off] = round_tf32(acc - hi);
         } else {
-          dst[0] = geo.tf32 ? round_tf32(acc) : acc;
+          dst[0] = TF ? round_tf32(acc) : acc;
         }
         dst += plane;
       }
@@ -959,7 +960,7 @@ typedef size_t (*SmallCSmem)(int);
 struct XformK {
   int z;
   uint64_t za[2], zb[2];   // skipped entries of Aᵀ / Bᵀ (zero_masks.h)
-  InputK ik;
+  InputK ik[3];           // by Geo::tf32
   OutputK ok[3];          // by epilogue: y only / ReLU / ReLU + pool
   SmallCK sck;            // fused C <= kSmcC kernel (NULL: not compiled for this shape)
   SmallCSmem sck_smem;
@@ -982,7 +983,9 @@ XformK make_xform_k() {
     v.za[w] = ZM<Z>::A(w);
     v.zb[w] = ZM<Z>::B(w);
   }
-  v.ik = input_kernel<M, R, Z>;
+  v.ik[0] = input_kernel<M, R, Z, 0>;
+  v.ik[1] = input_kernel<M, R, Z, 1>;
+  v.ik[2] = input_kernel<M, R, Z, 2>;
   v.ok[0] = output_kernel<M, R, Z, 0>;
   v.ok[1] = output_kernel<M, R, Z, 1>;
   v.ok[2] = output_kernel<M, R, Z, 2>;
@@ -1186,7 +1189,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   if (!smallc) {
     const int cpt = (m + r - 1) > 8 ? 4 : 1;   // = in_cpt<N>() of the kernel
     const long long tot = (long long)(g.Cp / cpt) * g.Tp;
-    const auto ik = xk.ik;
+    const auto ik = xk.ik[g.tf32];
     const dim3 igrid((unsigned)((tot + tpb - 1) / tpb));
     timed_launch("layer_input", stream, [&] {
       if (pdl)
