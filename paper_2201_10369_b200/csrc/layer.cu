@@ -502,9 +502,9 @@ __device__ __forceinline__ void unpack2(u64 v, float& lo, float& hi) {
 
 // one row (P of the tile, image row h) of one output channel: y and / or the fused
 // activation; identical to K4's epilogue
-template <int M, int P>
+template <int M, int P, int EP>
 __device__ __forceinline__ void smc_emit_row(const float (&yr)[M], float (&prev)[M], int h, int tx, float* yk, float* ak,
-                                             int pool, bool pairs, const Geo& geo, int Hp, int Wp) {
+                                             bool pairs, const Geo& geo, int Hp, int Wp) {
   const int wmax = geo.Wo - tx * M;
   if (yk != nullptr && h < geo.Ho) {
     float* row = yk + (long long)h * geo.Wo + tx * M;
@@ -518,8 +518,8 @@ __device__ __forceinline__ void smc_emit_row(const float (&yr)[M], float (&prev)
         if (s < wmax) row[s] = yr[s];
     }
   }
-  if (ak != nullptr) {
-    if (pool == 1) {
+  if (EP != 0 && ak != nullptr) {
+    if (EP == 1) {
       if (h < geo.Ho) {
         float* row = ak + (long long)h * geo.Wo + tx * M;
         if (pairs) {   // Wo even and both base pointers 8-byte aligned (checked by the kernel)
@@ -547,9 +547,9 @@ __device__ __forceinline__ void smc_emit_row(const float (&yr)[M], float (&prev)
   }
 }
 
-template <int M, int N, int Z, int P>
+template <int M, int N, int Z, int P, int EP>
 __device__ __forceinline__ void smc_rows(const u64 (&t3)[M][N], const LayerMats& mt, float (&prev0)[M], float (&prev1)[M],
-                                         int ty, int tx, float* yk0, float* yk1, float* ak0, float* ak1, int pool,
+                                         int ty, int tx, float* yk0, float* yk1, float* ak0, float* ak1, bool has1,
                                          bool pairs, const Geo& geo, int Hp, int Wp) {
   if constexpr (P < M) {
     float y0[M], y1[M];
@@ -562,9 +562,9 @@ __device__ __forceinline__ void smc_rows(const u64 (&t3)[M][N], const LayerMats&
       unpack2(acc, y0[s], y1[s]);
     }
     const int h = ty * M + P;
-    smc_emit_row<M, P>(y0, prev0, h, tx, yk0, ak0, pool, pairs, geo, Hp, Wp);
-    if (yk1 != nullptr || ak1 != nullptr) smc_emit_row<M, P>(y1, prev1, h, tx, yk1, ak1, pool, pairs, geo, Hp, Wp);
-    smc_rows<M, N, Z, P + 1>(t3, mt, prev0, prev1, ty, tx, yk0, yk1, ak0, ak1, pool, pairs, geo, Hp, Wp);
+    smc_emit_row<M, P, EP>(y0, prev0, h, tx, yk0, ak0, pairs, geo, Hp, Wp);
+    if (has1) smc_emit_row<M, P, EP>(y1, prev1, h, tx, yk1, ak1, pairs, geo, Hp, Wp);
+    smc_rows<M, N, Z, P + 1, EP>(t3, mt, prev0, prev1, ty, tx, yk0, yk1, ak0, ak1, has1, pairs, geo, Hp, Wp);
   }
 }
 
@@ -575,12 +575,14 @@ size_t smc_smem(int C) {
   return (size_t)C * N * N * kSmcT * sizeof(float) + (size_t)(kSmcKG / 2) * C * smc_nnp<N>() * sizeof(u64);
 }
 
-template <int M, int R, int Z>
+template <int M, int R, int Z, int EP>   // EP: K4's epilogue modes (y only / ReLU / ReLU + pool)
 __global__ void __launch_bounds__(kSmcT, 2) smallc_kernel(const float* __restrict__ x, const float* __restrict__ U,
                                                          float* __restrict__ y, Geo geo,
-                                                         const __grid_constant__ LayerMats mt, float* __restrict__ act,
-                                                         int pool) {
+                                                         const __grid_constant__ LayerMats mt, float* __restrict__ act_in,
+                                                         int) {
   constexpr int N = M + R - 1, NN = N * N, NNP = smc_nnp<N>();
+  constexpr int pool = EP == 2 ? 2 : 1;
+  float* const act = EP == 0 ? nullptr : act_in;
   extern __shared__ __align__(16) float smc_sm[];
   float* sV = smc_sm;                                                       // [C][NN][kSmcT]
   u64* sU = reinterpret_cast<u64*>(smc_sm + (size_t)geo.C * NN * kSmcT);    // [kSmcKG/2][C][NNP]
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(kSmcT, 2) smallc_kernel(const float* __restric
     float* ak0 = act ? act + ((long long)img * geo.K + k) * asz : nullptr;
     float* ak1 = (act && k1) ? ak0 + asz : nullptr;
     float prev0[M], prev1[M];
-    smc_rows<M, N, Z, 0>(t3, mt, prev0, prev1, ty, tx, yk0, yk1, ak0, ak1, pool, pairs, geo, Hp, Wp);
+    smc_rows<M, N, Z, 0, EP>(t3, mt, prev0, prev1, ty, tx, yk0, yk1, ak0, ak1, k1, pairs, geo, Hp, Wp);
   }
 }
 
@@ -962,7 +964,7 @@ struct XformK {
   uint64_t za[2], zb[2];   // skipped entries of Aᵀ / Bᵀ (zero_masks.h)
   InputK ik[3];           // by Geo::tf32
   OutputK ok[3];          // by epilogue: y only / ReLU / ReLU + pool
-  SmallCK sck;            // fused C <= kSmcC kernel (NULL: not compiled for this shape)
+  SmallCK sck[3];         // fused C <= kSmcC kernel by epilogue (NULL: not compiled for this shape)
   SmallCSmem sck_smem;
 };
 
@@ -989,10 +991,12 @@ XformK make_xform_k() {
   v.ok[0] = output_kernel<M, R, Z, 0>;
   v.ok[1] = output_kernel<M, R, Z, 1>;
   v.ok[2] = output_kernel<M, R, Z, 2>;
-  v.sck = nullptr;
+  v.sck[0] = v.sck[1] = v.sck[2] = nullptr;
   v.sck_smem = nullptr;
   if constexpr (R == 3 && M + R - 1 <= 8) {   // the first layers of the 3 x 3 stacks
-    v.sck = smallc_kernel<M, R, Z>;
+    v.sck[0] = smallc_kernel<M, R, Z, 0>;
+    v.sck[1] = smallc_kernel<M, R, Z, 1>;
+    v.sck[2] = smallc_kernel<M, R, Z, 2>;
     v.sck_smem = smc_smem<M + R - 1>;
   }
   return v;
@@ -1157,7 +1161,7 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   // C <= 4 (RGB first layers): K2 + K3 + K4 fused in one kernel after K1 (smallc_kernel);
   // WINO_LAYER_NO_SMALLC=1 forces the unfused pipeline (A/B measurements, parity tests)
   const bool no_smallc = std::getenv("WINO_LAYER_NO_SMALLC") != nullptr;
-  const bool smallc = !tf32 && !no_smallc && C <= kSmcC && xk.sck != nullptr && xk.sck_smem(C) <= 200 * 1024;
+  const bool smallc = !tf32 && !no_smallc && C <= kSmcC && xk.sck[0] != nullptr && xk.sck_smem(C) <= 200 * 1024;
   // Unfused fp32 path: K1 -> K2 -> K3 -> K4 as a programmatic-dependent-launch chain on
   // `stream` (lpdl_wait above; K2 runs beside K1 without a side stream, K3 / K4 become
   // resident while their predecessor drains).  The timing hook records events between the
@@ -1178,10 +1182,10 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   if (forked) cudaEventRecord(side.join, fs);
   if (smallc) {
     const size_t smem = xk.sck_smem(C);
-    const auto sck = xk.sck;
+    const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
+    const auto sck = xk.sck[fuse ? (pool == 2 ? 2 : 1) : 0];
     cudaFuncSetAttribute((const void*)sck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)((g.T + kSmcT - 1) / kSmcT), (unsigned)((K + kSmcKG - 1) / kSmcKG));
-    const bool fuse = act != nullptr && (pool == 1 || m % 2 == 0);
     timed_launch("layer_smallc", stream,
                  [&] { sck<<<grid, kSmcT, smem, stream>>>(x, U, y, g, mt, fuse ? act : nullptr, pool); });
     launches++;
