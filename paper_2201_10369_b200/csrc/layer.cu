@@ -1167,7 +1167,11 @@ int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, 
   // resident while their predecessor drains).  The timing hook records events between the
   // launches, which would serialise them, so with the hook on (and for the TF32 variants,
   // whose GEMM has no wait) the kernels are launched plainly with K1 on the side stream.
-  const bool pdl = !tf32 && !smallc && !timing_enabled() && std::getenv("WINO_LAYER_NO_PDL") == nullptr;
+  // n > 8: the input transform runs one 256-thread CTA per SM in < 2 waves; started behind
+  // K1's CTAs instead of racing them from another stream it takes an extra wave (configs[3]
+  // n = 10: 0.205 ms plain, 0.215 ms chained), so those shapes keep the side stream.
+  const bool pdl = !tf32 && !smallc && !timing_enabled() && (m + r - 1) <= 8 &&
+                   std::getenv("WINO_LAYER_NO_PDL") == nullptr;
   SideStream& side = side_stream();
   bool forked = !smallc && !pdl && side.ok && cudaEventRecord(side.fork, stream) == cudaSuccess &&
                 cudaStreamWaitEvent(side.s, side.fork, 0) == cudaSuccess;
