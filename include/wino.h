@@ -107,12 +107,19 @@ int wino_points_to_matrices(int m, int r, const double* points, int n,
  * ascending-c fmaf chain per (k, tile, Winograd position), no split, no TF32.
  * Output is bit-identical to the oracle's O5 layer.  N == 0 or K == 0 (empty output) is a
  * successful no-op (nothing enqueued, statistics untouched); C, H, W >= 1 are required.
- * Asynchronous on `stream`; the filter
- * transform runs on a library-owned side stream (one per host thread and device) forked
- * from and joined back to `stream` with events, so the call stays stream-ordered and
- * graph-capturable.  wino_conv2d_workspace_bytes() is large enough for every variant of
+ * Asynchronous on `stream` and stream-ordered: the kernels of one call form a
+ * programmatic-dependent-launch chain on `stream` (n <= 8), or the filter transform runs on
+ * a library-owned side stream (one per host thread and device) forked from and joined back
+ * to `stream` with events (n > 8, the variants of (2c), the timing hook on,
+ * WINO_LAYER_NO_PDL=1); C <= 4 layers run the transforms and the contraction in one fused
+ * kernel (same bits).  wino_conv2d_workspace_bytes() is large enough for every variant of
  * (2c) as well. */
 size_t wino_conv2d_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m);
+/* Diagnostic: which contraction kernel this shape runs in the parity path (2): the CTA tile
+ * as 1000 * k_rows + t_cols (128128, 64128 when K <= 64, 128064 when the narrow tile needs
+ * fewer waves), 1 for the fused C <= 4 kernel, 0 for invalid or unsupported
+ * arguments.  Host only; the tests use it to make sure every variant is exercised. */
+int wino_conv2d_gemm_tile(int N, int C, int H, int W, int K, int r, int pad, int m);
 int wino_conv2d_fp32(const float* x, const float* w, float* y,
                      int N, int C, int H, int W, int K, int r, int pad, int m,
                      const double* points, void* workspace, size_t workspace_bytes,

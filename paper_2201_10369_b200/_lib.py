@@ -25,6 +25,7 @@ SIGNATURES = [
     ("wino_supported", ctypes.c_int, [ctypes.c_int] * 3),
     ("wino_points_to_matrices", ctypes.c_int, [ctypes.c_int, ctypes.c_int, _d, ctypes.c_int, _d, _d, _d]),
     ("wino_conv2d_workspace_bytes", _sz, [ctypes.c_int] * 8),
+    ("wino_conv2d_gemm_tile", ctypes.c_int, [ctypes.c_int] * 8),
     ("wino_conv2d_fp32", ctypes.c_int,
      [_vp, _vp, _vp] + [ctypes.c_int] * 8 + [_d, _vp, _sz, _vp, _vp, _vp]),
     ("wino_conv2d_fp32_ex", ctypes.c_int,

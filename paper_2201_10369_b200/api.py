@@ -133,6 +133,11 @@ def wino_conv2d_relu_pool_fp32(x, w, y, act, pad: int, m: int, points: Sequence[
     check(st, "wino_conv2d_relu_pool_fp32")
 
 
+def wino_conv2d_gemm_tile(N: int, C: int, H: int, W: int, K: int, r: int, pad: int, m: int) -> int:
+    """Diagnostic: 1000 * k_rows + t_cols of the contraction's CTA tile, 1 for the fused C <= 4 kernel."""
+    return int(load().wino_conv2d_gemm_tile(N, C, H, W, K, r, pad, m))
+
+
 def wino_relu_pool_fp32(x, y, pool: int, stream=None) -> None:
     """y = maxpool_pool(ReLU(x)); x [N,C,H,W], y [N,C,H/pool,W/pool] fp32 CUDA tensors."""
     import torch

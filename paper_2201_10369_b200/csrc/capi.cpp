@@ -164,6 +164,12 @@ size_t wino_conv2d_workspace_bytes(int N, int C, int H, int W, int K, int r, int
   return layer_workspace_bytes(N, C, H, W, K, r, pad, m);
 }
 
+int wino_conv2d_gemm_tile(int N, int C, int H, int W, int K, int r, int pad, int m) {
+  if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || r < 1 || m < 1 || pad < 0) return 0;
+  if (H + 2 * pad < r || W + 2 * pad < r || !layer_supported(m, r)) return 0;
+  return layer_gemm_tile(N, C, H, W, K, r, pad, m);
+}
+
 int wino_conv2d_fp32(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
                      int m, const double* points, void* workspace, size_t workspace_bytes, double* d_sums,
                      double* d_maxs, void* stream) {

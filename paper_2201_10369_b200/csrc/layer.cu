@@ -1129,6 +1129,16 @@ size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, 
                   ws_layout(make_geo(N, C, H, W, K, r, pad, m, 2)).total);
 }
 
+// which kernel layer_launch picks for the parity path (wino_conv2d_gemm_tile)
+int layer_gemm_tile(int N, int C, int H, int W, int K, int r, int pad, int m) {
+  const LayerCfg* cfg = find_layer(m, r);
+  if (!cfg) return 0;
+  const bool no_smallc = std::getenv("WINO_LAYER_NO_SMALLC") != nullptr;
+  if (!no_smallc && C <= kSmcC && cfg->xk[0].sck[0] != nullptr && cfg->xk[0].sck_smem(C) <= 200 * 1024) return 1;
+  const Geo g = make_geo(N, C, H, W, K, r, pad, m, 0);
+  return g.Kp == 64 ? 64128 : 128000 + g.bn;
+}
+
 int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K, int r, int pad,
                  int m, const float* AT, const float* G, const float* BT, void* workspace, size_t ws_bytes,
                  double* d_sums, double* d_maxs, unsigned flags, cudaStream_t stream, float* act, int pool) {

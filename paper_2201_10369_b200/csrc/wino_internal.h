@@ -35,6 +35,7 @@ int sweep_launch(int dims, int m, int r, const double* point_sets, int* cand_sta
 
 int layer_supported(int m, int r);
 size_t layer_workspace_bytes(int N, int C, int H, int W, int K, int r, int pad, int m);
+int layer_gemm_tile(int N, int C, int H, int W, int K, int r, int pad, int m);
 int layer_launch(const float* x, const float* w, float* y, int N, int C, int H, int W, int K,
                  int r, int pad, int m, const float* AT, const float* G, const float* BT,
                  void* workspace, size_t ws_bytes, double* d_sums, double* d_maxs,

@@ -190,3 +190,18 @@ def test_layer_empty_batch_and_validation_without_device():
     assert st == 3                                   # point validation still applies
     st = L.wino_conv2d_fp32_ex(p, p, p, 0, 8, 16, 16, 8, 3, 1, 2, pp, None, 0, None, None, 8, None)
     assert st == 1                                   # unknown flag
+
+
+def test_contraction_kernel_choice_vgg_shapes():
+    """wino_conv2d_gemm_tile (host only): the configs[4] VGG-16 x64 layers pick the fused
+    first-layer kernel, 64-row tiles for K = 64, and the 128 x 64 tile exactly where it saves
+    a wave (28 x 28: 11 waves instead of 12; 14 x 14: 4 instead of 5)."""
+    from paper_2201_10369_b200 import api
+    t = lambda C, K, H: api.wino_conv2d_gemm_tile(64, C, H, H, K, 3, 1, 6)
+    assert t(3, 64, 224) == 1
+    assert t(64, 64, 224) == 64128
+    assert t(64, 128, 112) == 128128 and t(256, 256, 56) == 128128
+    assert t(256, 512, 28) == 128064 and t(512, 512, 14) == 128064
+    assert api.wino_conv2d_gemm_tile(32, 256, 56, 56, 256, 3, 1, 6) == 128128   # configs[2]
+    assert api.wino_conv2d_gemm_tile(0, 3, 8, 8, 8, 3, 1, 6) == 0 and t(8, 8, 9) != 0
+    assert api.wino_conv2d_gemm_tile(1, 8, 8, 8, 8, 4, 1, 6) == 0               # no F(6,4) layer kernel
