@@ -256,3 +256,34 @@ def test_every_contraction_kernel_variant(N, C, H, K, m, pts, tile):
     assert np.array_equal(y, y_ref)
     s_ref, m_ref = _oracle_stats(x, w, 1, y_ref)
     _check_stats(s, mx, s_ref, m_ref)
+
+
+@pytest.mark.parametrize("C,K,H,tile,imgs,pool", [
+    (512, 512, 14, 128064, (0, 37, 63), 1),    # conv5_x: T = 576 -> 4 waves of 128 x 64 tiles
+    (512, 512, 14, 128064, (11,), 2),          # conv5_3: the same with the fused pool
+    (256, 512, 28, 128064, (0, 63), 1),        # conv4_1: T = 1600 -> 11 waves instead of 12
+    (3, 64, 224, 1, (63,), 1),                 # conv1_1: the fused C = 3 kernel, 92,416 tiles
+    (64, 64, 224, 64128, (5,), 2),             # conv1_2: 64-row GEMM tiles, fused pool
+])
+def test_vgg_layers_full_batch_sampled_images(C, K, H, tile, imgs, pool):
+    """BASELINE.json configs[4] layer shapes at the full batch of 64 in the launch
+    configuration the VGG-16 run uses (the narrow GEMM tile / the fused first-layer kernel
+    are chosen only at these sizes); sampled images recomputed by the oracle, ReLU
+    activation included."""
+    import torch
+    from oracle import network as ON
+    from paper_2201_10369_b200 import api
+    N, m = 64, 6
+    assert api.wino_conv2d_gemm_tile(N, C, H, H, K, 3, 1, m) == tile
+    pts = OP.n8_cd(2.0, 1.003)
+    x, w = synth.layer_inputs(N, C, H, H, K, 3, "normal", "he", seed=21)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    ws = torch.empty(api.wino_conv2d_workspace_bytes(N, C, H, H, K, 3, 1, m), dtype=torch.uint8, device="cuda")
+    y = torch.empty((N, K, H, H), dtype=torch.float32, device="cuda")
+    act = torch.empty((N, K, H // pool, H // pool), dtype=torch.float32, device="cuda")
+    api.wino_conv2d_relu_pool_fp32(xd, wd, y, act, 1, m, pts, ws, pool)
+    torch.cuda.synchronize()
+    for img in imgs:
+        y_ref = ref.conv2d_wino(x, w, 1, m, pts, n_lo=img, n_hi=img + 1)
+        assert np.array_equal(y[img].cpu().numpy(), y_ref[img])
+        assert np.array_equal(act[img].cpu().numpy(), ON.relu_pool(y_ref[img:img + 1], pool == 2)[0])
